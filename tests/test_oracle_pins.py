@@ -1,0 +1,356 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (no GPU).
+
+Each test pins oracle/ to something other than itself: SPEC/PAPER worked
+examples (tests/golden/spec_examples.json, cited), exact rational brute force
+on tiny inputs (fractions.Fraction), closed forms (chunking invariance of the
+committed state), library routines (torch's bf16 rounding), and invariants
+of the serving contract.
+"""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import numerics as nm
+from oracle.planner import MODE_FULL, MODE_PHASE, MODE_SERIAL, Event, OraclePlanner, validate_group
+from oracle.run import ok_commits, run_batched, run_sequential
+from oracle.state import READ, WRITE, ContractError, StateTable
+from workload import traces as T
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ---------------------------------------------------------------- bf16 storage
+def test_round_bf16_matches_torch_library_rounding():
+    rs = np.random.default_rng(1)
+    x = np.concatenate([rs.standard_normal(20000).astype(np.float32) * 10.0 ** rs.integers(-6, 6, 20000),
+                        np.array([1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -1.0 - 2 ** -8, 2 ** -130, 3e38],
+                                 dtype=np.float32)]).astype(np.float32)
+    ref = torch.from_numpy(x).to(torch.bfloat16).to(torch.float64).numpy()
+    got = nm.round_bf16(x.astype(np.float64))
+    assert np.array_equal(got, ref)
+
+
+def test_round_bf16_hand_values():
+    # 1 + 2^-8 is a tie between 1 and 1 + 2^-7: ties to even -> 1.0
+    assert nm.round_bf16(np.array([1.0 + 2 ** -8]))[0] == 1.0
+    # 1 + 3*2^-8 ties between 1+2^-7 (odd) and 1+2^-6 (even) -> 1 + 2^-6
+    assert nm.round_bf16(np.array([1.0 + 3 * 2 ** -8]))[0] == 1.0 + 2 ** -6
+    assert nm.round_bf16(np.array([1.0 + 2 ** -8 + 2 ** -20]))[0] == 1.0 + 2 ** -7
+
+
+# ---------------------------------------------------------------- READ
+def _frac_read(W, S, z):
+    dm, dff = len(W), len(W[0])
+    return [sum((Fraction(W[i][j]) + Fraction(S[i][j])) * Fraction(z[j]) for j in range(dff))
+            for i in range(dm)]
+
+
+def test_read_exact_rational_brute_force_nonsquare():
+    rs = np.random.default_rng(2)
+    dm, dff = 3, 5          # non-square: a transposed operand cannot type-check
+    W = rs.integers(-8, 8, (dm, dff)) / 16.0
+    S = rs.integers(-8, 8, (dm, dff)) / 32.0
+    z = rs.integers(-8, 8, dff) / 8.0
+    y = nm.apply_read(W, S, z)
+    ref = _frac_read(W.tolist(), S.tolist(), z.tolist())
+    assert [Fraction(v) for v in y] == ref
+
+
+def test_read_spec_examples_rule1():
+    for k in ("read_identity_zero", "read_identity_I"):
+        g = GOLD[k]
+        y = nm.apply_read(None, np.array(g["W"], float), np.array(g["x"], float), rule=g["rule"])
+        assert y.tolist() == g["y"], g["cite"]
+
+
+def test_read_base_only_when_delta_zero_and_delta_only_when_base_zero():
+    rs = np.random.default_rng(3)
+    W = rs.integers(-4, 4, (4, 6)) / 4.0
+    z = rs.integers(-4, 4, 6) / 4.0
+    zero = np.zeros_like(W)
+    assert np.array_equal(nm.apply_read(W, zero, z), nm.apply_read(zero, W, z))
+    assert not np.array_equal(nm.apply_read(W, W, z), nm.apply_read(W, zero, z)) or not z.any()
+
+
+# ---------------------------------------------------------------- WRITE
+def test_write_exact_rational_brute_force():
+    rs = np.random.default_rng(4)
+    dm, dff, C = 3, 4, 5
+    S = rs.integers(-8, 8, (dm, dff)) / 16.0
+    Z = rs.integers(-4, 4, (C, dff)) / 4.0
+    V = rs.integers(-4, 4, (C, dm)) / 4.0
+    eta = 2.0 ** -4
+    cand = nm.boundary_update(S, Z, V, eta, "fp32")
+    for i in range(dm):
+        for j in range(dff):
+            ref = Fraction(S[i, j]) + Fraction(eta) * sum(Fraction(V[t, i]) * Fraction(Z[t, j]) for t in range(C))
+            assert Fraction(cand[i, j]) == ref
+
+
+def test_write_spec_examples_rule1():
+    g = GOLD["update_outer"]
+    eta = float(np.float32(g["eta"]))
+    # tokens all equal to m give evidence mean m
+    Z = np.array([g["m"], g["m"]], float)
+    cand = nm.boundary_update(np.array(g["W"], float), Z, None, eta, "fp32", rule=1)
+    assert np.all(cand == np.float32(g["W_new_each"])), g["cite"]
+    g = GOLD["update_zero"]
+    cand = nm.boundary_update(np.array(g["W"], float), np.array([g["m"]], float), None, 0.01, "fp32", rule=1)
+    assert np.all(cand == 0.0)
+    g = GOLD["mean_evidence"]
+    cand = nm.boundary_update(np.zeros((2, 2)), np.array(g["tokens"], float), None, 1.0, "fp32", rule=1)
+    assert np.array_equal(cand, np.outer(g["m"], g["m"])), g["cite"]
+
+
+def test_write_two_boundary_toy_spec_s564():
+    # W = η(m1 m1ᵀ + m2 m2ᵀ) after two boundaries from W = 0
+    eta = 2.0 ** -3
+    Z1 = np.array([[1.0, 0.5], [0.0, 0.5]])
+    Z2 = np.array([[-1.0, 1.0], [0.5, 0.0]])
+    W1 = nm.boundary_update(np.zeros((2, 2)), Z1, None, eta, "fp32", rule=1)
+    W2 = nm.boundary_update(W1, Z2, None, eta, "fp32", rule=1)
+    m1, m2 = Z1.mean(0), Z2.mean(0)
+    assert np.array_equal(W2, eta * (np.outer(m1, m1) + np.outer(m2, m2)))
+
+
+def test_write_bf16_storage_is_library_rounding_of_exact_candidate():
+    rs = np.random.default_rng(5)
+    S = nm.round_bf16(rs.standard_normal((4, 6)) * 0.01)
+    Z = rs.integers(-4, 4, (8, 6)) / 4.0
+    V = rs.integers(-4, 4, (8, 4)) / 4.0
+    eta = float(np.float32(0.01))
+    exact = S + eta * (V.T @ Z)                     # exact in fp64 at these sizes? check via fp32 path
+    ref = torch.from_numpy(exact.astype(np.float32)).to(torch.bfloat16).double().numpy()
+    got = nm.boundary_update(S, Z, V, eta, "bf16")
+    # rounding fp64 directly vs fp64->fp32->bf16 can differ only on double-rounding ties
+    assert np.mean(got == ref) > 0.99 and nm.normwise_rel_err(got, exact) < 2 ** -8
+
+
+def test_committed_state_closed_form_chunking_invariance():
+    """S_k = S_0 + η Σ_{committed t} v_t z_tᵀ, independent of chunking (SURVEY §8(c) pins).
+
+    fp32 storage with dyadic inputs keeps every partial sum exact, so the
+    chunked state must equal one unchunked sum bit for bit.
+    """
+    for C in (1, 2, 4, 8):
+        tr = T.uniform_small(n_streams=2, n_layers=2, d_model=3, d_ff=5, chunk=C, n_steps=16, dtype="fp32")
+        tr = tr.replace(eta=2.0 ** -4)
+        # dyadic inputs: override generator with small integers / 4
+        rs = np.random.default_rng(6)
+        X = rs.integers(-4, 5, (2, 16, 2, 5)) / 4.0
+        Vt = rs.integers(-4, 5, (2, 16, 2, 3)) / 4.0
+        tab = StateTable(2, 3, 5, C, "fp32", [np.zeros((3, 5))] * 2, tr.eta)
+        for s in range(2):
+            tab.alloc(s)
+            for p in range(16):
+                eff = tab.next_effect(s)
+                tab.apply(s, p, list(X[s, p]), list(Vt[s, p]))
+                if eff == WRITE:
+                    tab.write_group([s])
+            for l in range(2):
+                closed = tr.eta * Vt[s, :, l, :].T @ X[s, :, l, :]
+                assert np.array_equal(tab.owners[s].S[l], closed)
+            assert tab.version(s) == 16 // C
+
+
+# ---------------------------------------------------------------- state contract
+def _tiny_table(C=2, dtype="fp32"):
+    return StateTable(1, 2, 3, C, dtype, [np.zeros((2, 3))], 0.5)
+
+
+def test_state_contract_spec_examples():
+    tab = _tiny_table()
+    assert tab.alloc(1) == 0
+    with pytest.raises(ContractError):
+        tab.alloc(1)
+    for r in range(2, 9):
+        tab.alloc(r)
+    assert all(tab.version(r) == 0 for r in range(1, 9))
+    z, v = [np.array([1.0, 0, 1])], [np.array([1.0, -1])]
+    assert tab.next_effect(1) == READ
+    tab.apply(1, 0, z, v)
+    assert tab.version(1) == 0                                  # S:72 READ preserves version
+    assert tab.next_effect(1) == WRITE
+    S_before = tab.owners[1].S[0].copy()
+    tab.apply(1, 1, z, v)
+    with pytest.raises(ContractError):
+        tab.write_group([1], fail=True)                         # failed write: nothing changes
+    assert tab.version(1) == 0 and np.array_equal(tab.owners[1].S[0], S_before) and tab.tail_len(1) == 2
+    assert tab.write_group([1]) == [1]
+    assert tab.tail_len(1) == 0
+    tab.snapshot(1)
+    snap = tab.owners[1].S[0].copy()
+    tab.apply(1, 2, z, v)
+    tab.apply(1, 3, z, v)
+    tab.write_group([1])
+    assert tab.version(1) == 2                                  # S:90 / S:99
+    assert tab.rollback(1) == 1
+    assert np.array_equal(tab.owners[1].S[0], snap) and tab.tail_len(1) == 0
+    assert tab.rollback(1) == 1                                 # checkpoint retained
+    with pytest.raises(ContractError):
+        tab.rollback(2)
+    tab.fork(1, 99)
+    assert tab.version(99) == 1
+    tab.apply(99, 0, z, v)
+    tab.apply(99, 1, z, v)
+    tab.write_group([99])
+    assert tab.version(99) == 2 and tab.version(1) == 1 and np.array_equal(tab.owners[1].S[0], snap)
+
+
+def test_group_write_is_atomic_and_owner_local():
+    tab = _tiny_table()
+    for r in (1, 2, 3):
+        tab.alloc(r)
+        for p in range(2):
+            tab.apply(r, p, [np.array([1.0, 2, 3])], [np.array([r * 1.0, 1])])
+    before = {r: tab.owners[r].S[0].copy() for r in (1, 2, 3)}
+    with pytest.raises(ContractError):
+        tab.write_group([1, 2], fail=True)
+    assert [tab.version(r) for r in (1, 2, 3)] == [0, 0, 0]
+    tab.write_group([1, 2])
+    assert [tab.version(r) for r in (1, 2, 3)] == [1, 1, 0]
+    assert np.array_equal(tab.owners[3].S[0], before[3])        # commit exclusivity
+    assert not np.array_equal(tab.owners[1].S[0], tab.owners[2].S[0])   # no aliasing
+    with pytest.raises(ContractError):
+        tab.write_group([3, 3])                                 # μ injective
+
+
+# ---------------------------------------------------------------- census and versions
+def test_census_uniform_trace_paper_p573():
+    g = GOLD["census_uniform"]
+    tr = T.uniform_small(n_streams=g["streams"], n_layers=1, d_model=2, d_ff=2, chunk=g["chunk"],
+                         n_steps=g["decode"], dtype="fp32")
+    rec = run_batched(tr, keep_outputs=False)
+    assert rec.census[READ] == g["reads"] and rec.census[WRITE] == g["writes"], g["cite"]
+    assert set(rec.versions.values()) == {GOLD["versions_uniform"]["final_version"]}
+
+
+def test_versions_all_update_trace():
+    g = GOLD["versions_all_update"]
+    tr = T.uniform_small(n_streams=g["streams"], n_layers=1, d_model=2, d_ff=2, chunk=g["chunk"],
+                         n_steps=g["decode"], dtype="fp32")
+    rec = run_batched(tr, keep_outputs=False)
+    assert rec.census[WRITE] == g["writes"] and set(rec.versions.values()) == {g["final_version"]}
+
+
+def test_config1_final_versions_and_log():
+    tr = T.config1_tiny()
+    rec = run_batched(tr)
+    assert [rec.versions[0], rec.versions[1]] == GOLD["config1_final_versions"]["versions"]
+    fails = [c for c in rec.commits if c[4] == "failed"]
+    assert {(c[0], c[1]) for c in fails} == {(0, 11), (1, 11)}        # group-atomic failure
+    assert all(c[2] == c[3] for c in fails)                            # v intact on failure
+    rb = [c for c in rec.commits if c[4] == "rolled_back"]
+    assert rb == [(1, 8, 2, 1, "rolled_back")]
+
+
+# ---------------------------------------------------------------- sequential == batched
+@pytest.mark.parametrize("mode", [MODE_SERIAL, MODE_PHASE, MODE_FULL])
+@pytest.mark.parametrize("w", [0, 2, 5])
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_sequential_equals_batched_bit_exact(mode, w, dtype):
+    tr = T.uniform_small(n_streams=5, n_layers=2, d_model=8, d_ff=12, chunk=4, n_steps=13, dtype=dtype,
+                         w=w, mode=mode, offsets=(0, 1, 3, 2, 0), delta0="rng", v0=7,
+                         controls={(1, 2): ["snapshot"], (1, 5): ["rollback"], (2, 0): ["fail"],
+                                   (4, 3): ["fail"], (3, 9): ["snapshot", "rollback"]})
+    tr = tr.replace(B=3)
+    a, b = run_sequential(tr), run_batched(tr)
+    assert a.outputs.keys() == b.outputs.keys()
+    for k in a.outputs:
+        assert np.array_equal(a.outputs[k], b.outputs[k]), k
+    assert a.versions == b.versions
+    for s in a.state:
+        for l in range(tr.n_layers):
+            assert np.array_equal(a.state[s][l], b.state[s][l])
+    assert ok_commits(a) == ok_commits(b)
+    assert a.census == b.census
+    # Eq. 4 bounded waiting, phase separation, injective μ on every issued group
+    for (issue, eff, ss, ready) in b.plan:
+        assert len(set(ss)) == len(ss)
+        assert all(0 <= issue - r <= tr.w for r in ready)
+        if mode == MODE_SERIAL:
+            assert len(ss) == 1
+        if mode == MODE_PHASE and eff == WRITE:
+            assert len(ss) == 1
+        assert len(ss) <= tr.B
+
+
+# ---------------------------------------------------------------- planner
+def _ev(r, eff=READ, v=0, ready=0, shape=0):
+    return Event(r, eff, 0, shape, 0, v, ready)
+
+
+def test_planner_spec_examples():
+    V = lambda r: 0
+    p = OraclePlanner(8, 0)
+    g, rej = p.plan([_ev(r) for r in range(8)], 0, V)
+    assert [len(x.owners) for x in g] == GOLD["planner_8_reads"]["groups"] and not rej
+    p = OraclePlanner(8, 0)
+    g, _ = p.plan([_ev(r) for r in range(6)] + [_ev(r, WRITE) for r in range(6, 8)], 0, V)
+    assert sorted(len(x.owners) for x in g) == sorted(GOLD["planner_6r_2w"]["groups"])
+    assert all(len({x for x in grp.owners}) == len(grp.owners) for grp in g)
+    assert {grp.effect for grp in g} == {READ, WRITE}
+    gw = GOLD["planner_wait"]
+    p = OraclePlanner(gw["B"], gw["w"])
+    issued = None
+    evs = [_ev(r, ready=gw["ready"]) for r in range(gw["n"])]
+    for clock in range(gw["ready"], gw["ready"] + 10):
+        g, _ = p.plan(evs if clock == gw["ready"] else [], clock, V)
+        if g:
+            issued = g[0].issue_step
+            break
+    assert issued == gw["issue"]
+
+
+def test_planner_rejects_stale_and_collisions_and_allows_mixed_versions():
+    V = {1: 3, 2: 1, 3: 5}.get
+    p = OraclePlanner(8, 0)
+    g, rej = p.plan([_ev(1, v=2), _ev(2, v=1), _ev(3, v=5), _ev(3, v=5)], 0, V)
+    assert [e.owner for e in rej] == [1, 3]          # stale and duplicate owner
+    assert g[0].owners == [2, 3]                     # different numeric versions co-issue
+    assert validate_group(g[0], V, [1, 5]) is None
+    assert validate_group(g[0], V, [1, 4]) == "VERSION_MISMATCH"
+
+
+def test_planner_property_eq3_eq4_random():
+    """≥1000 random event sets: homogeneous κ, injective μ, version match, bounded wait."""
+    rs = np.random.default_rng(7)
+    for trial in range(1000):
+        B, w = int(rs.integers(1, 6)), int(rs.integers(0, 4))
+        p = OraclePlanner(B, w, int(rs.integers(0, 3)))
+        Vt = {r: int(rs.integers(0, 3)) for r in range(12)}
+        waiting = {}
+        for clock in range(8):
+            evs = []
+            for r in range(12):
+                if r not in waiting and rs.random() < 0.5:
+                    v = Vt[r] if rs.random() < 0.9 else Vt[r] + 1
+                    evs.append(Event(r, int(rs.integers(0, 2)), 0, int(rs.integers(0, 2)), 0, v, clock))
+            groups, rej = p.plan(evs, clock, Vt.get)
+            for e in evs:
+                if e not in rej:
+                    waiting[e.owner] = e
+            for g in groups:
+                assert len(set(g.owners)) == len(g.owners) and 1 <= len(g.owners) <= B
+                for r in g.owners:
+                    e = waiting.pop(r)
+                    assert (e.effect, e.shape_id) == (g.effect, g.shape_id)
+                    assert e.version == Vt[r]
+                    assert 0 <= clock - e.ready_step <= w
+            for e in rej:
+                assert e.version != Vt[e.owner] or e.owner in waiting
+        # drain: every waiting event issues within w more steps
+        for clock in range(8, 8 + w + 1):
+            for g in p.plan([], clock, Vt.get)[0]:
+                for r in g.owners:
+                    waiting.pop(r)
+        assert not waiting
+
+
+def test_normwise_metric():
+    assert nm.normwise_rel_err(np.array([1.0, 2.0]), np.array([1.0, 2.0])) == 0.0
+    assert nm.normwise_rel_err(np.array([1.0, 2.1]), np.array([1.0, 2.0])) == pytest.approx(0.05)
