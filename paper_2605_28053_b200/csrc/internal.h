@@ -1,0 +1,70 @@
+// Internal declarations shared by the host library (pool/planner/api) and
+// the sm_100a kernels.  Not part of the public ABI (that is include/tttstate.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace ttt {
+
+constexpr int kMaxReadMembers = 8;     // members per READ launch (X rows staged in smem)
+constexpr int kMaxGroup = 256;         // members per group (planner B cap)
+
+// a3 + a4: decode READ over one layer for ≤ kMaxReadMembers members.
+struct ReadParams {
+  const void *X, *Vt, *resid;
+  void *Y;
+  const void *w_down_l;          // [d_model][d_ff] of this layer
+  const void *slots;             // pool slot array base
+  long long slot_elems;          // elements per slot (L * d_model * d_ff)
+  long long layer_off;           // layer * d_model * d_ff
+  const int *sel;                // device active-slot selector per owner index
+  void *tailZ, *tailV;           // tail ring bases
+  long long tz_owner, tv_owner;  // elements per owner (L*C*d_ff, L*C*d_model)
+  long long tz_layer, tv_layer;  // layer offset in elements (layer*C*d_ff, layer*C*d_model)
+  float *Pbase, *Pdelta;         // [kMaxReadMembers][d_model] partial sums
+  int *tickets;                  // [d_model] arrival counters (self-resetting)
+  int n, d_model, d_ff;
+  int owner_idx[kMaxReadMembers];
+  int x_row[kMaxReadMembers], v_row[kMaxReadMembers], y_row[kMaxReadMembers];
+  int tail_pos[kMaxReadMembers];
+};
+
+// a5: chunk update of one layer for every member (shadow slot <- ΔW_v + η VᵀZ).
+struct WriteParams {
+  void *slots;
+  long long slot_elems, layer_off;
+  const int *sel;
+  const void *tailZ, *tailV;
+  long long tz_owner, tv_owner, tz_layer, tv_layer;
+  float eta;
+  int *fail_flag;
+  int n, d_model, d_ff, C;
+  int owner_idx[kMaxGroup];
+};
+
+// a6: group-atomic publish.
+struct CommitParams {
+  int *sel;
+  unsigned long long *version;
+  int *fail_flag;      // device-detected failure flag of the current group (reset here)
+  int *fail_count;     // cumulative device-detected failed groups (read by tttstate_sync)
+  int forced_fail;     // injected failure (host-known)
+  int n;
+  int owner_idx[kMaxGroup];
+};
+
+int device_sm_count();
+cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s);
+cudaError_t launch_write_simt(int dtype, const WriteParams &p, cudaStream_t s);
+cudaError_t launch_write_tc(const WriteParams &p, cudaStream_t s);   // bf16, tcgen05
+bool write_tc_supported(int d_model, int d_ff, int C);
+cudaError_t launch_commit(const CommitParams &p, cudaStream_t s);
+cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s);
+cudaError_t launch_set_state(int *sel, unsigned long long *version, int idx, int sel_v,
+                             unsigned long long ver, cudaStream_t s);
+
+void count_launch(int n = 1);
+
+}  // namespace ttt

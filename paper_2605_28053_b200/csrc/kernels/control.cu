@@ -1,0 +1,88 @@
+// a6 / a7 — commit, checkpoint copy and state set kernels.
+//
+// Commit: "Commit publishes a dirty state
+// as owner r's next version only after the WRITE group succeeds ... The
+// version counter changes here, not inside the backend update".  Group-atomic
+// (SURVEY.md §8(c) reading vi): one CTA reads the group's
+// fail flag once, then every member flips its active slot and bumps its
+// version, or none does.  No payload bytes move (the dirty candidate already
+// sits in the shadow slot), replacing the paper's "selective commit" copy
+// kernel with an O(1)-per-owner publish.
+//
+// Checkpoint copy ("Checkpoint write", K5): a 16-byte vectorised
+// device copy used when a pinned checkpoint slot must be preserved, for
+// fork, and for rollback from the checkpoint pool.
+#include "../internal.h"
+
+namespace ttt {
+namespace {
+
+__global__ void commit_kernel(const CommitParams p) {
+  __shared__ int fail;
+  if (threadIdx.x == 0) fail = p.forced_fail | *reinterpret_cast<volatile int *>(p.fail_flag);
+  __syncthreads();
+  if (!fail) {
+    for (int b = threadIdx.x; b < p.n; b += blockDim.x) {
+      const int o = p.owner_idx[b];
+      p.sel[o] ^= 1;
+      p.version[o] += 1ull;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (fail && !p.forced_fail) atomicAdd(p.fail_count, 1);
+    *p.fail_flag = 0;
+  }
+}
+
+__global__ void copy_kernel(uint4 *__restrict__ dst, const uint4 *__restrict__ src, size_t n16) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+    dst[i] = a; dst[i + stride] = b; dst[i + 2 * stride] = c; dst[i + 3 * stride] = d;
+  }
+  for (; i < n16; i += stride) dst[i] = src[i];
+}
+
+__global__ void copy_tail_bytes(unsigned char *dst, const unsigned char *src, size_t n) {
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+__global__ void set_state_kernel(int *sel, unsigned long long *version, int idx, int s,
+                                 unsigned long long v) {
+  sel[idx] = s;
+  version[idx] = v;
+}
+
+}  // namespace
+
+cudaError_t launch_commit(const CommitParams &p, cudaStream_t s) {
+  commit_kernel<<<1, 256, 0, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+  const size_t n16 = bytes / 16;
+  if (n16) {
+    const int grid = device_sm_count() * 4;
+    copy_kernel<<<grid, 512, 0, s>>>(static_cast<uint4 *>(dst), static_cast<const uint4 *>(src), n16);
+    count_launch();
+  }
+  if (bytes % 16) {
+    copy_tail_bytes<<<1, 32, 0, s>>>(static_cast<unsigned char *>(dst) + n16 * 16,
+                                     static_cast<const unsigned char *>(src) + n16 * 16, bytes % 16);
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_state(int *sel, unsigned long long *version, int idx, int sel_v,
+                             unsigned long long ver, cudaStream_t s) {
+  set_state_kernel<<<1, 1, 0, s>>>(sel, version, idx, sel_v, ver);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ttt

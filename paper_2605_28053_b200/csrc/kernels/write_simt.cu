@@ -1,0 +1,121 @@
+// a5 — WRITE (BoundaryUpdate), SIMT fp32-FFMA version.
+//
+// PAPER: "the update reads owner r's committed version v and produces one
+// dirty candidate state for that owner. The candidate is invisible to later
+// READs until committed" (WRITE paragraph; Table 3 BoundaryUpdate
+// P:387-390).  Rule: SURVEY.md §8(c) reading i,
+//     ΔW̃_{v+1}[i][j] = ΔW_v[i][j] + η · Σ_{t<C} V_c[t][i] · Z_c[t][j].
+// The candidate goes to the owner's shadow slot (2·o + 1 − sel[o]); the
+// committed slot (2·o + sel[o]) is only read.  A non-finite candidate
+// element raises the group's device fail flag ("finite entries").
+//
+// This kernel is the true-fp32 path for σ.dtype = fp32 (BJ configs[0]
+// tolerance 1e-5 excludes tf32) and the fallback-free reference
+// design for bf16 storage when the tcgen05 kernel does not apply.  64×64
+// output tile per CTA, 4×4 per thread, K = C streamed through shared memory
+// in 32-token slices, fixed summation order t = 0..C−1.
+#include <cuda_bf16.h>
+
+#include <cmath>
+
+#include "../internal.h"
+
+namespace ttt {
+namespace {
+
+constexpr int TI = 64, TJ = 64, KT = 32, NT = 256;
+
+template <typename T>
+__device__ __forceinline__ float ld_f(const T *p);
+template <>
+__device__ __forceinline__ float ld_f<float>(const float *p) { return *p; }
+template <>
+__device__ __forceinline__ float ld_f<__nv_bfloat16>(const __nv_bfloat16 *p) { return __bfloat162float(*p); }
+
+template <typename T>
+__device__ __forceinline__ T st_cvt(float v);
+template <>
+__device__ __forceinline__ float st_cvt<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 st_cvt<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+template <typename T>
+__global__ void __launch_bounds__(NT) write_simt_kernel(const WriteParams p) {
+  __shared__ float Vs[KT][TI];
+  __shared__ float Zs[KT][TJ];
+  const int b = blockIdx.z;
+  const int o = p.owner_idx[b];
+  const int i0 = blockIdx.y * TI, j0 = blockIdx.x * TJ;
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  const int dm = p.d_model, dff = p.d_ff, C = p.C;
+  const T *Z = static_cast<const T *>(p.tailZ) + o * p.tz_owner + p.tz_layer;   // [C][d_ff]
+  const T *V = static_cast<const T *>(p.tailV) + o * p.tv_owner + p.tv_layer;   // [C][d_model]
+
+  float acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
+
+  for (int t0 = 0; t0 < C; t0 += KT) {
+    for (int idx = tid; idx < KT * TI; idx += NT) {
+      const int t = idx / TI, ii = idx % TI;
+      Vs[t][ii] = (t0 + t < C && i0 + ii < dm) ? ld_f(V + (size_t)(t0 + t) * dm + i0 + ii) : 0.f;
+    }
+    for (int idx = tid; idx < KT * TJ; idx += NT) {
+      const int t = idx / TJ, jj = idx % TJ;
+      Zs[t][jj] = (t0 + t < C && j0 + jj < dff) ? ld_f(Z + (size_t)(t0 + t) * dff + j0 + jj) : 0.f;
+    }
+    __syncthreads();
+    const int kt = min(KT, C - t0);
+    for (int t = 0; t < kt; ++t) {
+      float a[4], c[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = Vs[t][ty * 4 + q];
+        c[q] = Zs[t][tx * 4 + q];
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[r][q] = fmaf(a[r], c[q], acc[r][q]);
+    }
+    __syncthreads();
+  }
+
+  const long long src_slot = 2LL * o + p.sel[o];
+  const long long dst_slot = 2LL * o + 1 - p.sel[o];
+  const T *S = static_cast<const T *>(p.slots) + src_slot * p.slot_elems + p.layer_off;
+  T *D = static_cast<T *>(p.slots) + dst_slot * p.slot_elems + p.layer_off;
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = i0 + ty * 4 + r;
+    if (i >= dm) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + tx * 4 + q;
+      if (j >= dff) continue;
+      const size_t off = (size_t)i * dff + j;
+      const float cand = fmaf(p.eta, acc[r][q], ld_f(S + off));
+      const T st = st_cvt<T>(cand);
+      bad |= !isfinite(ld_f(&st));
+      D[off] = st;
+    }
+  }
+  if (bad) atomicOr(p.fail_flag, 1);
+}
+
+}  // namespace
+
+cudaError_t launch_write_simt(int dtype, const WriteParams &p, cudaStream_t s) {
+  dim3 grid((p.d_ff + TJ - 1) / TJ, (p.d_model + TI - 1) / TI, p.n);
+  if (dtype == 1)
+    write_simt_kernel<__nv_bfloat16><<<grid, NT, 0, s>>>(p);
+  else
+    write_simt_kernel<float><<<grid, NT, 0, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ttt

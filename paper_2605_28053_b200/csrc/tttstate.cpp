@@ -1,0 +1,616 @@
+// C-ABI implementation: TTTState pool (double-slot arena + host mirror),
+// READ/WRITE/commit enqueue with validation-before-side-effects, control
+// operations (snapshot / rollback / fork), sync and test hooks.
+//
+// Contract sources: ownership rule P:233-246; Eq. 2-3; StateView
+// P:346-352; primitives Table 3; Alg. 1 P:442-466;
+// SPEC state_core S:56-146 and executor S:355-409 for error conventions.
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_set>
+
+#include "pool.h"
+
+namespace ttt {
+
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+static std::atomic<int> g_write_impl{0};
+
+void count_launch(int n) { g_launches += n; }
+
+int device_sm_count() {
+  static int cached_dev = -1, cached = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    cached_dev = dev;
+  }
+  return cached;
+}
+
+static ttt_status fail(ttt_status s, const std::string &msg) {
+  g_last_error = std::string(tttstate_status_name(s)) + ": " + msg;
+  return s;
+}
+
+static ttt_status cuda_fail(cudaError_t e, const char *what) {
+  return fail(TTT_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(expr)                                   \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr);  \
+  } while (0)
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt) {
+  const size_t es = s.dtype == TTT_BF16 ? 2 : 4;
+  const size_t E = (size_t)s.d_model * s.d_ff;
+  const size_t slot = (size_t)s.n_layers * E * es;
+  Layout L;
+  size_t off = 0;
+  L.slots = off;   off = align_up(off + slot * (2 * (size_t)max_owners + n_ckpt), 1024);
+  L.tailZ = off;   off = align_up(off + (size_t)max_owners * s.n_layers * s.chunk * s.d_ff * es, 1024);
+  L.tailV = off;   off = align_up(off + (size_t)max_owners * s.n_layers * s.chunk * s.d_model * es, 1024);
+  L.sel = off;     off = align_up(off + (size_t)max_owners * 4, 256);
+  L.ver = off;     off = align_up(off + (size_t)max_owners * 8, 256);
+  L.flags = off;   off = align_up(off + 64, 256);
+  L.P = off;       off = align_up(off + 2 * (size_t)kMaxReadMembers * s.d_model * 4, 256);
+  L.tickets = off; off = align_up(off + (size_t)s.d_model * 4, 1024);
+  L.total = off;
+  return L;
+}
+
+static ttt_status check_shape(const ttt_shape *s) {
+  if (!s) return fail(TTT_E_INVALID_ARG, "null shape");
+  if (s->backend != TTT_FAST_WEIGHT) return fail(TTT_E_SHAPE, "only the fast-weight backend (τ=0) is built");
+  if (s->dtype != TTT_BF16 && s->dtype != TTT_FP32) return fail(TTT_E_SHAPE, "dtype");
+  if (s->d_model <= 0 || s->d_ff <= 0 || s->chunk <= 0 || s->n_layers <= 0)
+    return fail(TTT_E_SHAPE, "non-positive dimension");
+  const int vec = s->dtype == TTT_BF16 ? 8 : 4;
+  if (s->d_ff % vec) return fail(TTT_E_SHAPE, "d_ff must be a multiple of 8 (bf16) / 4 (fp32)");
+  if (s->d_model % 4) return fail(TTT_E_SHAPE, "d_model must be a multiple of 4");
+  if (s->rule != 0) return fail(TTT_E_SHAPE, "only rule 0 (chunk outer-product sum) is built on the GPU");
+  return TTT_OK;
+}
+
+}  // namespace ttt
+
+using namespace ttt;
+
+// ---------------------------------------------------------------- helpers
+namespace {
+
+ttt_status find_owner(ttt_pool *p, uint64_t owner, OwnerRec **out) {
+  auto it = p->owners.find(owner);
+  if (it == p->owners.end()) return fail(TTT_E_UNKNOWN_OWNER, "owner " + std::to_string(owner));
+  *out = &it->second;
+  return TTT_OK;
+}
+
+// Key homogeneity (Eq. 3) against this pool, known owners, injective μ.
+ttt_status check_group(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec *> &recs) {
+  if (!p || !g || !g->owner_map) return fail(TTT_E_INVALID_ARG, "null pool/group");
+  if (g->n < 1 || g->n > kMaxGroup) return fail(TTT_E_CAPACITY, "group size must be in [1, 256]");
+  if (g->backend != p->sh.backend || g->shape_id != p->shape_id || g->placement != p->placement)
+    return fail(TTT_E_MIXED_KEY, "group key (τ,σ,π) does not match the pool");
+  if (g->effect != TTT_READ && g->effect != TTT_WRITE) return fail(TTT_E_INVALID_ARG, "effect");
+  std::unordered_set<uint64_t> seen;
+  recs.resize(g->n);
+  for (int b = 0; b < g->n; ++b) {
+    if (!seen.insert(g->owner_map[b]).second)
+      return fail(TTT_E_OWNER_COLLISION, "owner " + std::to_string(g->owner_map[b]) + " twice in μ");
+    ttt_status st = find_owner(p, g->owner_map[b], &recs[b]);
+    if (st != TTT_OK) return st;
+  }
+  return TTT_OK;
+}
+
+void clear_applied(OwnerRec &r) {
+  std::fill(r.applied.begin(), r.applied.end(), 0);
+  r.n_applied = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *tttstate_last_error(void) { return g_last_error.c_str(); }
+
+const char *tttstate_status_name(ttt_status s) {
+  switch (s) {
+    case TTT_OK: return "TTT_OK";
+    case TTT_E_UNKNOWN_OWNER: return "TTT_E_UNKNOWN_OWNER";
+    case TTT_E_DUPLICATE_OWNER: return "TTT_E_DUPLICATE_OWNER";
+    case TTT_E_VERSION_MISMATCH: return "TTT_E_VERSION_MISMATCH";
+    case TTT_E_OWNER_COLLISION: return "TTT_E_OWNER_COLLISION";
+    case TTT_E_MIXED_KEY: return "TTT_E_MIXED_KEY";
+    case TTT_E_DOUBLE_WRITE: return "TTT_E_DOUBLE_WRITE";
+    case TTT_E_TAIL_NOT_FULL: return "TTT_E_TAIL_NOT_FULL";
+    case TTT_E_NO_CHECKPOINT: return "TTT_E_NO_CHECKPOINT";
+    case TTT_E_WRITE_FAILED: return "TTT_E_WRITE_FAILED";
+    case TTT_E_POOL_FULL: return "TTT_E_POOL_FULL";
+    case TTT_E_SHAPE: return "TTT_E_SHAPE";
+    case TTT_E_TAIL_FULL: return "TTT_E_TAIL_FULL";
+    case TTT_E_WRONG_EFFECT: return "TTT_E_WRONG_EFFECT";
+    case TTT_E_NOT_APPLIED: return "TTT_E_NOT_APPLIED";
+    case TTT_E_ALREADY_APPLIED: return "TTT_E_ALREADY_APPLIED";
+    case TTT_E_CAPACITY: return "TTT_E_CAPACITY";
+    case TTT_E_INVALID_ARG: return "TTT_E_INVALID_ARG";
+    case TTT_E_CUDA: return "TTT_E_CUDA";
+    case TTT_E_NO_DEVICE: return "TTT_E_NO_DEVICE";
+  }
+  return "TTT_E_?";
+}
+
+int64_t tttstate_launch_count(void) { return g_launches.load(); }
+
+int32_t tttstate_set_write_impl(int32_t impl) { return g_write_impl.exchange(impl); }
+
+// ---------------------------------------------------------------- pool
+ttt_status tttstate_pool_bytes(const ttt_shape *shape, int32_t max_owners, int32_t n_ckpt, size_t *bytes_out) {
+  ttt_status st = check_shape(shape);
+  if (st != TTT_OK) return st;
+  if (max_owners < 1 || n_ckpt < 0 || !bytes_out) return fail(TTT_E_INVALID_ARG, "max_owners/n_ckpt/out");
+  *bytes_out = compute_layout(*shape, max_owners, n_ckpt).total;
+  return TTT_OK;
+}
+
+ttt_status tttstate_pool_create(const ttt_shape *shape, int32_t shape_id, int32_t placement, int32_t max_owners,
+                                int32_t n_ckpt, void *dev_arena, size_t arena_bytes, const void *w_down,
+                                ttt_pool **out) {
+  ttt_status st = check_shape(shape);
+  if (st != TTT_OK) return st;
+  if (!out || max_owners < 1 || n_ckpt < 0) return fail(TTT_E_INVALID_ARG, "out/max_owners/n_ckpt");
+  Layout lay = compute_layout(*shape, max_owners, n_ckpt);
+  if (dev_arena) {
+    if (arena_bytes < lay.total) return fail(TTT_E_INVALID_ARG, "arena too small");
+    if (reinterpret_cast<uintptr_t>(dev_arena) % 1024) return fail(TTT_E_INVALID_ARG, "arena not 1024-aligned");
+    if (!w_down) return fail(TTT_E_INVALID_ARG, "w_down is required for rule 0");
+  }
+  auto *p = new ttt_pool();
+  p->sh = *shape;
+  p->shape_id = shape_id;
+  p->placement = placement;
+  p->max_owners = max_owners;
+  p->n_ckpt = n_ckpt;
+  p->host_only = dev_arena == nullptr;
+  p->arena = static_cast<unsigned char *>(dev_arena);
+  p->arena_bytes = arena_bytes;
+  p->w_down = w_down;
+  p->esize = shape->dtype == TTT_BF16 ? 2 : 4;
+  p->E = (long long)shape->d_model * shape->d_ff;
+  p->slot_elems = p->E * shape->n_layers;
+  p->tz_owner = (long long)shape->n_layers * shape->chunk * shape->d_ff;
+  p->tv_owner = (long long)shape->n_layers * shape->chunk * shape->d_model;
+  p->lay = lay;
+  for (int i = max_owners - 1; i >= 0; --i) p->free_idx.push_back(i);
+  for (int c = n_ckpt - 1; c >= 0; --c) p->free_ckpt.push_back(c);
+  if (!p->host_only) {
+    cudaError_t e = cudaMemset(p->arena + lay.sel, 0, lay.total - lay.sel);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      delete p;
+      return cuda_fail(e, "pool tables init");
+    }
+  }
+  *out = p;
+  return TTT_OK;
+}
+
+ttt_status tttstate_pool_destroy(ttt_pool *pool) {
+  delete pool;
+  return TTT_OK;
+}
+
+ttt_status tttstate_alloc(ttt_pool *p, uint64_t owner, const void *init, uint64_t v0, uint64_t *v_out,
+                          void *stream) {
+  if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
+  if (p->owners.count(owner)) return fail(TTT_E_DUPLICATE_OWNER, "owner " + std::to_string(owner));
+  if (p->free_idx.empty()) return fail(TTT_E_POOL_FULL, "no free owner slot");
+  if (init && p->host_only) return fail(TTT_E_NO_DEVICE, "init bytes need a device pool");
+  const int idx = p->free_idx.back();
+  if (!p->host_only) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (init)
+      CUDA_TRY(cudaMemcpyAsync(p->slot_ptr(2LL * idx), init, p->slot_bytes(), cudaMemcpyDeviceToDevice, s));
+    else
+      CUDA_TRY(cudaMemsetAsync(p->slot_ptr(2LL * idx), 0, p->slot_bytes(), s));
+    CUDA_TRY(launch_set_state(p->d_sel(), p->d_ver(), idx, 0, v0, s));
+  }
+  p->free_idx.pop_back();
+  OwnerRec r;
+  r.idx = idx;
+  r.version = v0;
+  r.applied.assign(p->sh.n_layers, 0);
+  p->owners.emplace(owner, std::move(r));
+  if (v_out) *v_out = v0;
+  return TTT_OK;
+}
+
+ttt_status tttstate_free(ttt_pool *p, uint64_t owner) {
+  if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
+  OwnerRec *r;
+  ttt_status st = find_owner(p, owner, &r);
+  if (st != TTT_OK) return st;
+  if (r->ckpt_pool >= 0) p->free_ckpt.push_back(r->ckpt_pool);
+  p->free_idx.push_back(r->idx);
+  p->owners.erase(owner);
+  return TTT_OK;
+}
+
+ttt_status tttstate_tail_load(ttt_pool *p, uint64_t owner, int32_t n, const void *Z, const void *V,
+                              void *stream) {
+  if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
+  OwnerRec *r;
+  ttt_status st = find_owner(p, owner, &r);
+  if (st != TTT_OK) return st;
+  if (n < 0 || n > p->sh.chunk - 1) return fail(TTT_E_INVALID_ARG, "n must be in [0, C-1]");
+  if (r->tail_len != 0 || r->n_applied != 0) return fail(TTT_E_TAIL_FULL, "tail not empty");
+  if (n == 0) return TTT_OK;
+  if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  if (!Z || !V) return fail(TTT_E_INVALID_ARG, "null Z/V");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const ttt_shape &sh = p->sh;
+  for (int l = 0; l < sh.n_layers; ++l) {
+    unsigned char *tz = p->arena + p->lay.tailZ + ((size_t)r->idx * p->tz_owner + (size_t)l * sh.chunk * sh.d_ff) * p->esize;
+    unsigned char *tv = p->arena + p->lay.tailV + ((size_t)r->idx * p->tv_owner + (size_t)l * sh.chunk * sh.d_model) * p->esize;
+    CUDA_TRY(cudaMemcpyAsync(tz, static_cast<const unsigned char *>(Z) + (size_t)l * n * sh.d_ff * p->esize,
+                             (size_t)n * sh.d_ff * p->esize, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(tv, static_cast<const unsigned char *>(V) + (size_t)l * n * sh.d_model * p->esize,
+                             (size_t)n * sh.d_model * p->esize, cudaMemcpyDeviceToDevice, s));
+  }
+  r->tail_len = n;
+  return TTT_OK;
+}
+
+ttt_status tttstate_version(ttt_pool *p, uint64_t owner, uint64_t *v_out) {
+  if (!p || !v_out) return fail(TTT_E_INVALID_ARG, "null arg");
+  OwnerRec *r;
+  ttt_status st = find_owner(p, owner, &r);
+  if (st != TTT_OK) return st;
+  *v_out = r->version;
+  return TTT_OK;
+}
+
+ttt_status tttstate_tail_len(ttt_pool *p, uint64_t owner, int32_t *len_out) {
+  if (!p || !len_out) return fail(TTT_E_INVALID_ARG, "null arg");
+  OwnerRec *r;
+  ttt_status st = find_owner(p, owner, &r);
+  if (st != TTT_OK) return st;
+  *len_out = r->tail_len;
+  return TTT_OK;
+}
+
+ttt_status tttstate_next_event(ttt_pool *p, uint64_t owner, int64_t clock, ttt_event *out) {
+  if (!p || !out) return fail(TTT_E_INVALID_ARG, "null arg");
+  OwnerRec *r;
+  ttt_status st = find_owner(p, owner, &r);
+  if (st != TTT_OK) return st;
+  out->owner = owner;
+  out->effect = r->tail_len == p->sh.chunk - 1 ? TTT_WRITE : TTT_READ;   // reading ii
+  out->backend = p->sh.backend;
+  out->shape_id = p->shape_id;
+  out->placement = p->placement;
+  out->expected_version = r->version;
+  out->ready_step = clock;
+  return TTT_OK;
+}
+
+ttt_status validate_group(ttt_pool *p, const ttt_group *g, const uint64_t *expected_versions) {
+  std::vector<OwnerRec *> recs;
+  ttt_status st = check_group(p, g, recs);
+  if (st != TTT_OK) return st;
+  if (expected_versions)
+    for (int b = 0; b < g->n; ++b)
+      if (recs[b]->version != expected_versions[b])
+        return fail(TTT_E_VERSION_MISMATCH, "owner " + std::to_string(g->owner_map[b]));
+  return TTT_OK;
+}
+
+// ---------------------------------------------------------------- READ
+ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void *X, const int32_t *x_rows,
+                      const void *Vt, const int32_t *v_rows, void *Y, const int32_t *y_rows,
+                      const void *resid, void *stream) {
+  std::vector<OwnerRec *> recs;
+  ttt_status st = check_group(p, g, recs);
+  if (st != TTT_OK) return st;
+  const ttt_shape &sh = p->sh;
+  if (layer < 0 || layer >= sh.n_layers) return fail(TTT_E_SHAPE, "layer out of range");
+  for (int b = 0; b < g->n; ++b) {
+    OwnerRec &r = *recs[b];
+    const bool boundary = r.tail_len == sh.chunk - 1;
+    if (r.tail_len >= sh.chunk) return fail(TTT_E_TAIL_FULL, "owner " + std::to_string(g->owner_map[b]));
+    if ((g->effect == TTT_WRITE) != boundary)
+      return fail(TTT_E_WRONG_EFFECT, "owner " + std::to_string(g->owner_map[b]) +
+                                          (boundary ? " is at a chunk boundary (WRITE step)" : " is not at a boundary"));
+    if (r.applied[layer]) return fail(TTT_E_ALREADY_APPLIED, "owner " + std::to_string(g->owner_map[b]));
+  }
+  if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  if (!X || !Vt || !Y) return fail(TTT_E_INVALID_ARG, "null X/Vt/Y");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int per = std::max(1, std::min(kMaxReadMembers, (int)((200 * 1024) / ((size_t)sh.d_ff * p->esize))));
+  if ((size_t)sh.d_ff * p->esize > 200 * 1024) return fail(TTT_E_SHAPE, "d_ff row exceeds shared memory");
+  for (int b0 = 0; b0 < g->n; b0 += per) {
+    ReadParams rp{};
+    rp.X = X; rp.Vt = Vt; rp.resid = resid; rp.Y = Y;
+    rp.w_down_l = static_cast<const unsigned char *>(p->w_down) + (size_t)layer * p->E * p->esize;
+    rp.slots = p->arena + p->lay.slots;
+    rp.slot_elems = p->slot_elems;
+    rp.layer_off = (long long)layer * p->E;
+    rp.sel = p->d_sel();
+    rp.tailZ = p->arena + p->lay.tailZ;
+    rp.tailV = p->arena + p->lay.tailV;
+    rp.tz_owner = p->tz_owner; rp.tv_owner = p->tv_owner;
+    rp.tz_layer = (long long)layer * sh.chunk * sh.d_ff;
+    rp.tv_layer = (long long)layer * sh.chunk * sh.d_model;
+    rp.Pbase = reinterpret_cast<float *>(p->arena + p->lay.P);
+    rp.Pdelta = rp.Pbase + (size_t)kMaxReadMembers * sh.d_model;
+    rp.tickets = reinterpret_cast<int *>(p->arena + p->lay.tickets);
+    rp.n = std::min(per, g->n - b0);
+    rp.d_model = sh.d_model; rp.d_ff = sh.d_ff;
+    for (int k = 0; k < rp.n; ++k) {
+      const int b = b0 + k;
+      rp.owner_idx[k] = recs[b]->idx;
+      rp.x_row[k] = x_rows ? x_rows[b] : b;
+      rp.v_row[k] = v_rows ? v_rows[b] : b;
+      rp.y_row[k] = y_rows ? y_rows[b] : b;
+      rp.tail_pos[k] = recs[b]->tail_len;
+    }
+    cudaError_t e = launch_read_decode(sh.dtype, rp, s);
+    if (e != cudaSuccess) return cuda_fail(e, "read_decode launch");
+  }
+  for (int b = 0; b < g->n; ++b) {
+    recs[b]->applied[layer] = 1;
+    recs[b]->n_applied += 1;
+  }
+  return TTT_OK;
+}
+
+ttt_status tttstate_step_done(ttt_pool *p, const ttt_group *g) {
+  std::vector<OwnerRec *> recs;
+  ttt_status st = check_group(p, g, recs);
+  if (st != TTT_OK) return st;
+  if (g->effect != TTT_READ) return fail(TTT_E_WRONG_EFFECT, "step_done is for READ groups (write_commit ends a WRITE step)");
+  for (int b = 0; b < g->n; ++b)
+    if (recs[b]->n_applied != p->sh.n_layers)
+      return fail(TTT_E_NOT_APPLIED, "owner " + std::to_string(g->owner_map[b]));
+  for (int b = 0; b < g->n; ++b) {
+    recs[b]->tail_len += 1;
+    clear_applied(*recs[b]);
+  }
+  return TTT_OK;
+}
+
+// ---------------------------------------------------------------- WRITE + commit
+ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32_t *fail_mask,
+                        uint64_t *new_versions, void *stream) {
+  std::vector<OwnerRec *> recs;
+  ttt_status st = check_group(p, g, recs);
+  if (st != TTT_OK) return st;
+  const ttt_shape &sh = p->sh;
+  if (g->effect != TTT_WRITE) return fail(TTT_E_WRONG_EFFECT, "write_commit needs a WRITE group");
+  int need_evict = 0;
+  for (int b = 0; b < g->n; ++b) {
+    OwnerRec &r = *recs[b];
+    if (r.tail_len != sh.chunk - 1) return fail(TTT_E_TAIL_NOT_FULL, "owner " + std::to_string(g->owner_map[b]));
+    if (r.n_applied != sh.n_layers) return fail(TTT_E_NOT_APPLIED, "owner " + std::to_string(g->owner_map[b]));
+    if (r.has_ckpt && r.ckpt_pool < 0 && r.ckpt_sel == 1 - r.sel) ++need_evict;
+  }
+  if (need_evict > (int)p->free_ckpt.size()) return fail(TTT_E_POOL_FULL, "no free checkpoint slot for a pinned snapshot");
+  bool forced = false;
+  if (fail_mask)
+    for (int b = 0; b < g->n; ++b) forced |= (fail_mask[b / 32] >> (b % 32)) & 1u;
+  if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+  // preserve pinned checkpoints that sit in the shadow slot (K5 checkpoint write)
+  for (int b = 0; b < g->n; ++b) {
+    OwnerRec &r = *recs[b];
+    if (r.has_ckpt && r.ckpt_pool < 0 && r.ckpt_sel == 1 - r.sel) {
+      const int c = p->free_ckpt.back();
+      p->free_ckpt.pop_back();
+      CUDA_TRY(launch_copy(p->slot_ptr(2LL * p->max_owners + c), p->slot_ptr(2LL * r.idx + r.ckpt_sel),
+                           p->slot_bytes(), s));
+      r.ckpt_pool = c;
+    }
+  }
+  WriteParams wp{};
+  wp.slots = p->arena + p->lay.slots;
+  wp.slot_elems = p->slot_elems;
+  wp.sel = p->d_sel();
+  wp.tailZ = p->arena + p->lay.tailZ;
+  wp.tailV = p->arena + p->lay.tailV;
+  wp.tz_owner = p->tz_owner; wp.tv_owner = p->tv_owner;
+  wp.eta = eta;
+  wp.fail_flag = p->d_fail_flag();
+  wp.n = g->n; wp.d_model = sh.d_model; wp.d_ff = sh.d_ff; wp.C = sh.chunk;
+  for (int b = 0; b < g->n; ++b) wp.owner_idx[b] = recs[b]->idx;
+  const int impl = g_write_impl.load();
+  const bool use_tc = sh.dtype == TTT_BF16 && impl != 1 && write_tc_supported(sh.d_model, sh.d_ff, sh.chunk);
+  if (impl == 2 && !use_tc) return fail(TTT_E_SHAPE, "tcgen05 WRITE kernel does not support this shape");
+  for (int l = 0; l < sh.n_layers; ++l) {
+    wp.layer_off = (long long)l * p->E;
+    wp.tz_layer = (long long)l * sh.chunk * sh.d_ff;
+    wp.tv_layer = (long long)l * sh.chunk * sh.d_model;
+    cudaError_t e = use_tc ? launch_write_tc(wp, s) : launch_write_simt(sh.dtype, wp, s);
+    if (e != cudaSuccess) return cuda_fail(e, "write launch");
+  }
+  CommitParams cp{};
+  cp.sel = p->d_sel();
+  cp.version = p->d_ver();
+  cp.fail_flag = p->d_fail_flag();
+  cp.fail_count = p->d_fail_count();
+  cp.forced_fail = forced ? 1 : 0;
+  cp.n = g->n;
+  for (int b = 0; b < g->n; ++b) cp.owner_idx[b] = recs[b]->idx;
+  CUDA_TRY(launch_commit(cp, s));
+  if (forced) return fail(TTT_E_WRITE_FAILED, "injected failure: group not committed");
+  for (int b = 0; b < g->n; ++b) {
+    OwnerRec &r = *recs[b];
+    r.sel ^= 1;
+    r.version += 1;
+    r.tail_len = 0;
+    clear_applied(r);
+    if (new_versions) new_versions[b] = r.version;
+  }
+  return TTT_OK;
+}
+
+// ---------------------------------------------------------------- control
+ttt_status tttstate_snapshot(ttt_pool *p, uint64_t owner, void *stream) {
+  (void)stream;
+  if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
+  OwnerRec *r;
+  ttt_status st = find_owner(p, owner, &r);
+  if (st != TTT_OK) return st;
+  if (r->ckpt_pool >= 0) p->free_ckpt.push_back(r->ckpt_pool);
+  r->has_ckpt = true;
+  r->ckpt_v = r->version;
+  r->ckpt_sel = r->sel;      // pin the committed slot: O(1), no bytes move
+  r->ckpt_pool = -1;
+  return TTT_OK;
+}
+
+ttt_status rollback(ttt_pool *p, uint64_t owner, uint64_t *v_out, void *stream) {
+  if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
+  OwnerRec *r;
+  ttt_status st = find_owner(p, owner, &r);
+  if (st != TTT_OK) return st;
+  if (!r->has_ckpt) return fail(TTT_E_NO_CHECKPOINT, "owner " + std::to_string(owner));
+  if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int new_sel;
+  if (r->ckpt_pool < 0) {
+    new_sel = r->ckpt_sel;                       // re-point to the pinned slot
+  } else {
+    new_sel = 1 - r->sel;                        // copy the checkpoint back into the shadow slot
+    CUDA_TRY(launch_copy(p->slot_ptr(2LL * r->idx + new_sel), p->slot_ptr(2LL * p->max_owners + r->ckpt_pool),
+                         p->slot_bytes(), s));
+  }
+  CUDA_TRY(launch_set_state(p->d_sel(), p->d_ver(), r->idx, new_sel, r->ckpt_v, s));
+  r->sel = new_sel;
+  r->version = r->ckpt_v;
+  r->tail_len = 0;
+  clear_applied(*r);
+  if (v_out) *v_out = r->version;
+  return TTT_OK;
+}
+
+ttt_status tttstate_fork(ttt_pool *p, uint64_t src, uint64_t dst, void *stream) {
+  if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
+  OwnerRec *rs;
+  ttt_status st = find_owner(p, src, &rs);
+  if (st != TTT_OK) return st;
+  if (p->owners.count(dst)) return fail(TTT_E_DUPLICATE_OWNER, "owner " + std::to_string(dst));
+  if (p->free_idx.empty()) return fail(TTT_E_POOL_FULL, "no free owner slot");
+  if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int idx = p->free_idx.back();
+  CUDA_TRY(launch_copy(p->slot_ptr(2LL * idx), p->slot_ptr(2LL * rs->idx + rs->sel), p->slot_bytes(), s));
+  CUDA_TRY(launch_set_state(p->d_sel(), p->d_ver(), idx, 0, rs->version, s));
+  p->free_idx.pop_back();
+  OwnerRec r;
+  r.idx = idx;
+  r.version = rs->version;
+  r.applied.assign(p->sh.n_layers, 0);
+  p->owners.emplace(dst, std::move(r));
+  return TTT_OK;
+}
+
+ttt_status tttstate_sync(ttt_pool *p, void *stream, int32_t *n_failed_out) {
+  if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
+  if (n_failed_out) *n_failed_out = 0;
+  if (p->host_only) return TTT_OK;
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  int count = 0;
+  CUDA_TRY(cudaMemcpy(&count, p->d_fail_count(), sizeof(int), cudaMemcpyDeviceToHost));
+  if (count == p->fail_seen) return TTT_OK;
+  const int nf = count - p->fail_seen;
+  p->fail_seen = count;
+  std::vector<int> sel(p->max_owners);
+  std::vector<unsigned long long> ver(p->max_owners);
+  CUDA_TRY(cudaMemcpy(sel.data(), p->d_sel(), sel.size() * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(ver.data(), p->d_ver(), ver.size() * 8, cudaMemcpyDeviceToHost));
+  for (auto &kv : p->owners) {
+    OwnerRec &r = kv.second;
+    if (r.version != ver[r.idx] || r.sel != sel[r.idx]) {   // assumed committed, device refused
+      r.version = ver[r.idx];
+      r.sel = sel[r.idx];
+      r.tail_len = p->sh.chunk - 1;                           // tail retained for the retry
+      std::fill(r.applied.begin(), r.applied.end(), 1);
+      r.n_applied = p->sh.n_layers;
+    }
+  }
+  if (n_failed_out) *n_failed_out = nf;
+  return fail(TTT_E_WRITE_FAILED, std::to_string(nf) + " group(s) failed on the device");
+}
+
+// ---------------------------------------------------------------- test hooks
+ttt_status tttstate_read_slot_raw(ttt_pool *p, uint64_t owner, int32_t which, int32_t layer, void *host_dst,
+                                  void *stream) {
+  if (!p || !host_dst) return fail(TTT_E_INVALID_ARG, "null arg");
+  OwnerRec *r;
+  ttt_status st = find_owner(p, owner, &r);
+  if (st != TTT_OK) return st;
+  if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  if (layer < 0 || layer >= p->sh.n_layers) return fail(TTT_E_SHAPE, "layer");
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  long long slot;
+  if (which == 0 || which == 1) {
+    slot = 2LL * r->idx + which;
+  } else if (which == 2) {
+    if (r->ckpt_pool < 0) return fail(TTT_E_NO_CHECKPOINT, "checkpoint is not in the checkpoint pool");
+    slot = 2LL * p->max_owners + r->ckpt_pool;
+  } else {                                       // -1: committed slot per the device table
+    int dsel = 0;
+    CUDA_TRY(cudaMemcpy(&dsel, p->d_sel() + r->idx, 4, cudaMemcpyDeviceToHost));
+    slot = 2LL * r->idx + dsel;
+  }
+  CUDA_TRY(cudaMemcpy(host_dst, p->slot_ptr(slot) + (size_t)layer * p->E * p->esize, (size_t)p->E * p->esize,
+                      cudaMemcpyDeviceToHost));
+  return TTT_OK;
+}
+
+ttt_status tttstate_read_payload(ttt_pool *p, uint64_t owner, int32_t layer, void *host_dst, void *stream) {
+  return tttstate_read_slot_raw(p, owner, -1, layer, host_dst, stream);
+}
+
+ttt_status tttstate_read_tail(ttt_pool *p, uint64_t owner, int32_t layer, void *host_Z, void *host_V,
+                              void *stream) {
+  if (!p || !host_Z || !host_V) return fail(TTT_E_INVALID_ARG, "null arg");
+  OwnerRec *r;
+  ttt_status st = find_owner(p, owner, &r);
+  if (st != TTT_OK) return st;
+  if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  if (layer < 0 || layer >= p->sh.n_layers) return fail(TTT_E_SHAPE, "layer");
+  const ttt_shape &sh = p->sh;
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  CUDA_TRY(cudaMemcpy(host_Z, p->arena + p->lay.tailZ + ((size_t)r->idx * p->tz_owner + (size_t)layer * sh.chunk * sh.d_ff) * p->esize,
+                      (size_t)sh.chunk * sh.d_ff * p->esize, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(host_V, p->arena + p->lay.tailV + ((size_t)r->idx * p->tv_owner + (size_t)layer * sh.chunk * sh.d_model) * p->esize,
+                      (size_t)sh.chunk * sh.d_model * p->esize, cudaMemcpyDeviceToHost));
+  return TTT_OK;
+}
+
+ttt_status tttstate_device_version(ttt_pool *p, uint64_t owner, uint64_t *v_out, void *stream) {
+  if (!p || !v_out) return fail(TTT_E_INVALID_ARG, "null arg");
+  OwnerRec *r;
+  ttt_status st = find_owner(p, owner, &r);
+  if (st != TTT_OK) return st;
+  if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  unsigned long long v = 0;
+  CUDA_TRY(cudaMemcpy(&v, p->d_ver() + r->idx, 8, cudaMemcpyDeviceToHost));
+  *v_out = v;
+  return TTT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+"""Helpers for -m gpu parity tests: seeded host inputs uploaded to the device.
+
+Inputs come from workload/ only (shared seeded generator, no method math);
+expected values come from oracle/ only.  Nothing here computes the method.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import numerics as nm
+from paper_2605_28053_b200.serving import Engine, InputSource
+
+
+def to_dev(arr: np.ndarray, dtype: str, device) -> torch.Tensor:
+    if dtype == "bf16":
+        return torch.from_numpy(np.ascontiguousarray(arr).view(np.int16)).to(device).view(torch.bfloat16)
+    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to(device)
+
+
+def to_host_f64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().float().cpu().numpy().astype(np.float64)
+
+
+def bits_to_f64(a: np.ndarray, dtype: str) -> np.ndarray:
+    return nm.widen(a, dtype)
+
+
+class HostGenInputs(InputSource):
+    def __init__(self, tr, device, layers=None):
+        self.tr, self.dev = tr, device
+        self.layers = list(range(tr.n_layers)) if layers is None else layers
+        self.out = {}
+
+    def init_delta(self, s):
+        if self.tr.delta0 == "zero":
+            return None
+        return to_dev(np.stack([self.tr.delta0_of(s, l) for l in self.layers]), self.tr.dtype, self.dev)
+
+    def tail_prefill(self, s):
+        off = self.tr.offset(s)
+        if not off:
+            return None
+        ps = range(-off, 0)
+        Z = np.stack([np.stack([self.tr.x(s, p, l) for p in ps]) for l in self.layers])
+        V = np.stack([np.stack([self.tr.tgt(s, p, l) for p in ps]) for l in self.layers])
+        return off, to_dev(Z, self.tr.dtype, self.dev), to_dev(V, self.tr.dtype, self.dev)
+
+    def group_io(self, l, ss, ps):
+        tr = self.tr
+        X = to_dev(np.stack([tr.x(s, p, l) for s, p in zip(ss, ps)]), tr.dtype, self.dev)
+        Vt = to_dev(np.stack([tr.tgt(s, p, l) for s, p in zip(ss, ps)]), tr.dtype, self.dev)
+        Y = torch.empty(len(ss), tr.d_model, dtype=X.dtype, device=self.dev)
+        return X, None, Vt, None, Y, None
+
+    def on_output(self, l, ss, ps, Y, yr):
+        Yh = to_host_f64(Y)
+        for k, (s, p) in enumerate(zip(ss, ps)):
+            self.out[(s, p, l)] = Yh[k]
+
+
+def make_engine(tr, device="cuda", n_ckpt=4, max_owners=None, mode=None, B=None, w=None):
+    W = to_dev(np.stack([tr.w_down(l) for l in range(tr.n_layers)]), tr.dtype, device)
+    return Engine(tr.d_model, tr.d_ff, tr.chunk, tr.n_layers, tr.dtype,
+                  max_owners or tr.n_streams + 2, W, n_ckpt=n_ckpt,
+                  mode=tr.mode if mode is None else mode, B=tr.B if B is None else B,
+                  w=tr.w if w is None else w, eta=tr.eta)

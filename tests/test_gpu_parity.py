@@ -1,0 +1,179 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU fp64 oracle, same seeded inputs.
+
+Integers (owner ids, versions, commit/rollback log, census, group plan) must
+be bit-exact; activations and fast weights within BASELINE.json's tolerance
+(normwise max relative error 2e-2 bf16, 1e-5 fp32).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import numerics as nm
+from oracle.run import run_batched
+from workload import rng
+from workload import traces as T
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2605_28053_b200 import capi  # noqa: E402
+from paper_2605_28053_b200.serving import run_trace  # noqa: E402
+
+from .gpu_helpers import HostGenInputs, make_engine  # noqa: E402
+
+DEV = "cuda"
+
+
+def _compare(tr, ref, src, log, eng):
+    tol = nm.TOL[tr.dtype]
+    assert set(ref.outputs) == set(src.out)
+    worst = max(nm.normwise_rel_err(src.out[k], ref.outputs[k]) for k in ref.outputs)
+    assert worst <= tol, f"READ outputs: normwise err {worst} > {tol}"
+    assert log.versions == ref.versions
+    assert log.commits == ref.commits
+    assert log.census == ref.census
+    assert log.plan == ref.plan
+    werr = 0.0
+    for s in range(tr.n_streams):
+        for l in range(tr.n_layers):
+            got = capi.tttstate_read_payload(eng.pool, tr.owner(s), l, tr.d_model, tr.d_ff, tr.dtype)
+            werr = max(werr, nm.normwise_rel_err(nm.widen(got, tr.dtype), ref.state[s][l]))
+    assert werr <= tol, f"fast weights: normwise err {werr} > {tol}"
+    return worst, werr
+
+
+def _run(tr, **kw):
+    ref = run_batched(tr)
+    eng = make_engine(tr, DEV, **kw)
+    src = HostGenInputs(tr, DEV)
+    log = run_trace(eng, tr, src)
+    torch.cuda.synchronize()
+    return ref, src, log, eng
+
+
+def test_config1_tiny_fp32_parity():
+    tr = T.config1_tiny()
+    ref, src, log, eng = _run(tr)
+    _compare(tr, ref, src, log, eng)
+    assert [log.versions[0], log.versions[1]] == [4, 3]
+    assert log.fallbacks == 1
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_uniform_parity_ragged_and_split_groups(dtype):
+    # 9 members > 8 per READ launch (split), d_model/d_ff not tile multiples, 2 boundaries
+    tr = T.uniform_small(n_streams=9, n_layers=2, d_model=196, d_ff=328, chunk=8, n_steps=20, dtype=dtype,
+                         delta0="rng", v0=5, seed=3)
+    ref, src, log, eng = _run(tr)
+    _compare(tr, ref, src, log, eng)
+
+
+@pytest.mark.parametrize("mode,w", [(capi.MODE_SERIAL, 0), (capi.MODE_PHASE, 2), (capi.MODE_FULL, 0),
+                                    (capi.MODE_FULL, 3)])
+def test_bursty_controls_modes_parity(mode, w):
+    tr = T.uniform_small(n_streams=6, n_layers=2, d_model=64, d_ff=96, chunk=4, n_steps=14, dtype="bf16",
+                         delta0="rng", v0=2, offsets=(0, 1, 3, 2, 0, 3), mode=mode, w=w, seed=1,
+                         controls={(1, 2): ["snapshot"], (1, 5): ["rollback"], (2, 0): ["fail"],
+                                   (4, 3): ["fail"], (3, 9): ["snapshot"], (3, 11): ["rollback"],
+                                   (5, 0): ["snapshot"], (5, 13): ["rollback"]})
+    tr = tr.replace(B=4)
+    ref, src, log, eng = _run(tr)
+    _compare(tr, ref, src, log, eng)
+
+
+def test_all_update_chunk1_parity():
+    tr = T.uniform_small(n_streams=4, n_layers=1, d_model=64, d_ff=128, chunk=1, n_steps=10, dtype="bf16",
+                         delta0="rng", seed=2)
+    ref, src, log, eng = _run(tr)
+    _compare(tr, ref, src, log, eng)
+    assert set(log.versions.values()) == {10}
+
+
+def _slot(eng, tr, s, which, l=0):
+    return capi.tttstate_read_slot_raw(eng.pool, tr.owner(s), which, l, tr.d_model, tr.d_ff, tr.dtype)
+
+
+def test_read_immutability_failed_write_and_rollback_bytes():
+    tr = T.uniform_small(n_streams=2, n_layers=1, d_model=64, d_ff=96, chunk=2, n_steps=0, dtype="bf16",
+                         delta0="rng", seed=4)
+    eng = make_engine(tr, DEV, n_ckpt=1)
+    src = HostGenInputs(tr, DEV)
+    for s in range(2):
+        capi.tttstate_alloc(eng.pool, tr.owner(s), src.init_delta(s), 0)
+    pool, owners = eng.pool, [tr.owner(0), tr.owner(1)]
+    g_read = capi.Group(capi.READ, owners)
+    g_write = capi.Group(capi.WRITE, owners)
+
+    def step(p, group):
+        X, _, Vt, _, Y, _ = src.group_io(0, [0, 1], [p, p])
+        capi.read_apply(pool, group, 0, X, None, Vt, None, Y)
+
+    before = capi.tttstate_read_payload(pool, owners[0], 0, tr.d_model, tr.d_ff, "bf16")
+    step(0, g_read)
+    capi.tttstate_step_done(pool, g_read)
+    assert np.array_equal(before, capi.tttstate_read_payload(pool, owners[0], 0, tr.d_model, tr.d_ff, "bf16"))
+    with pytest.raises(capi.TTTError) as e:
+        step(1, g_read)                       # a WRITE step issued as READ
+    assert e.value.status == 13
+    step(1, g_write)
+    with pytest.raises(capi.TTTError) as e:
+        capi.write_commit(pool, g_write, tr.eta, [False, True])   # MidGroupWriteFail
+    assert e.value.status == capi.TTT_E_WRITE_FAILED
+    # versions and committed bytes intact for BOTH members; the shadow slot was written
+    assert [capi.tttstate_device_version(pool, o) for o in owners] == [0, 0]
+    assert np.array_equal(before, capi.tttstate_read_payload(pool, owners[0], 0, tr.d_model, tr.d_ff, "bf16"))
+    assert not np.array_equal(before, _slot(eng, tr, 0, 1))
+    capi.tttstate_snapshot(pool, owners[0])
+    assert capi.write_commit(pool, g_write, tr.eta) == [1, 1]
+    after1 = capi.tttstate_read_payload(pool, owners[0], 0, tr.d_model, tr.d_ff, "bf16")
+    assert not np.array_equal(before, after1)
+    # second commit writes into the pinned slot -> checkpoint moves to the pool first
+    for p in (2, 3):
+        g = g_read if p == 2 else g_write
+        step(p, g)
+        if p == 2:
+            capi.tttstate_step_done(pool, g)
+    capi.write_commit(pool, g_write, tr.eta)
+    assert capi.tttstate_version(pool, owners[0]) == 2
+    assert np.array_equal(before, _slot(eng, tr, 0, 2))            # checkpoint-pool copy is exact
+    assert capi.rollback(pool, owners[0]) == 0
+    assert capi.tttstate_device_version(pool, owners[0]) == 0
+    assert np.array_equal(before, capi.tttstate_read_payload(pool, owners[0], 0, tr.d_model, tr.d_ff, "bf16"))
+    assert capi.tttstate_version(pool, owners[1]) == 2              # owner-local
+    # fork isolation
+    capi.tttstate_fork(pool, owners[1], 77)
+    f0 = capi.tttstate_read_payload(pool, 77, 0, tr.d_model, tr.d_ff, "bf16")
+    assert np.array_equal(f0, capi.tttstate_read_payload(pool, owners[1], 0, tr.d_model, tr.d_ff, "bf16"))
+    assert capi.tttstate_version(pool, 77) == 2
+
+
+def test_device_detected_nonfinite_write_fails_group():
+    tr = T.uniform_small(n_streams=2, n_layers=1, d_model=64, d_ff=96, chunk=1, n_steps=0, dtype="fp32", seed=5)
+    eng = make_engine(tr, DEV)
+    pool, owners = eng.pool, [tr.owner(0), tr.owner(1)]
+    for o in owners:
+        capi.tttstate_alloc(pool, o)
+    g = capi.Group(capi.WRITE, owners)
+    X = torch.ones(2, tr.d_ff, device=DEV)
+    X[1, 3] = float("inf")
+    Vt = torch.ones(2, tr.d_model, device=DEV)
+    Y = torch.empty(2, tr.d_model, device=DEV)
+    capi.read_apply(pool, g, 0, X, None, Vt, None, Y)
+    capi.write_commit(pool, g, tr.eta)                 # optimistic host mirror
+    assert capi.tttstate_sync(pool) == 1               # reconciled
+    assert [capi.tttstate_version(pool, o) for o in owners] == [0, 0]
+    assert [capi.tttstate_device_version(pool, o) for o in owners] == [0, 0]
+    assert capi.tttstate_tail_len(pool, owners[0]) == 0 and capi.tttstate_next_event(pool, owners[0], 0).effect == 1
+
+
+def test_generator_device_matches_numpy():
+    for bf16 in (True, False):
+        for (t, o, l, p, n, amp) in [(rng.T_X, 1003, 2, 17, 1000, 1.0), (rng.T_W_DOWN, 0, 5, 0, 4099, 0.0101),
+                                     (rng.T_TGT, 7, 0, -3, 333, 1.0)]:
+            out = torch.empty(n, dtype=torch.bfloat16 if bf16 else torch.float32, device=DEV)
+            capi.gen_uniform(out, 11, t, o, l, p, n, amp, bf16)
+            ref = rng.gen(11, t, o, l, p, (n,), amp, "bf16" if bf16 else "fp32")
+            got = out.view(torch.int16).cpu().numpy().view(np.uint16) if bf16 else out.cpu().numpy()
+            assert np.array_equal(got, ref)

@@ -1,0 +1,99 @@
+"""Per-kernel microbenchmark at paper dims (d_model=2560, d_ff=9728, bf16): READ and WRITE.
+
+    python tools/microbench.py [--layers L] [--members B] [--iters N] [--write-impl 0|1|2]
+
+Times each C-ABI call with CUDA events on the launching stream and reports
+achieved HBM GB/s on ALGORITHMIC bytes against
+MEASURED_PEAKS.json.  Inputs are synthesised on the device (libttt_gen.so).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2605_28053_b200 import capi  # noqa: E402
+from paper_2605_28053_b200.serving import Engine  # noqa: E402
+from workload import rng  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--members", type=int, default=8)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--d-model", type=int, default=2560)
+    ap.add_argument("--d-ff", type=int, default=9728)
+    ap.add_argument("--chunk", type=int, default=128)
+    ap.add_argument("--write-impl", type=int, default=0)
+    a = ap.parse_args()
+    dm, dff, L, B, C = a.d_model, a.d_ff, a.layers, a.members, a.chunk
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    hbm = peaks["hbm_gbs"]
+    dev = torch.device("cuda")
+    W = torch.empty(L, dm, dff, dtype=torch.bfloat16, device=dev)
+    for l in range(L):
+        capi.gen_uniform(W[l], 0, rng.T_W_DOWN, 0, l, 0, dm * dff, rng.amp_inv_sqrt(dff), True)
+    eng = Engine(dm, dff, C, L, "bf16", B, W, n_ckpt=0, B=B)
+    owners = list(range(100, 100 + B))
+    d0 = torch.empty(L, dm, dff, dtype=torch.bfloat16, device=dev)
+    for o in owners:
+        for l in range(L):
+            capi.gen_uniform(d0[l], 0, rng.T_DELTA0, o, l, 0, dm * dff, rng.amp_inv_sqrt(dff), True)
+        capi.tttstate_alloc(eng.pool, o, d0, 0)
+    del d0
+    X = torch.empty(L, B, dff, dtype=torch.bfloat16, device=dev)
+    Vt = torch.empty(L, B, dm, dtype=torch.bfloat16, device=dev)
+    capi.gen_uniform(X, 0, rng.T_X, 0, 0, 0, X.numel(), 1.0, True)
+    capi.gen_uniform(Vt, 0, rng.T_TGT, 0, 0, 0, Vt.numel(), 1.0, True)
+    Y = torch.empty(L, B, dm, dtype=torch.bfloat16, device=dev)
+    g = capi.Group(capi.READ, owners)
+    gw = capi.Group(capi.WRITE, owners)
+    s = torch.cuda.current_stream()
+    res = {}
+
+    # READ: C-1 steps over all layers (fills the tail), timed per call
+    read_ms = []
+    for step in range(min(a.iters, C - 1)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for l in range(L):
+            capi.read_apply(eng.pool, g, l, X[l], None, Vt[l], None, Y[l], None, None, s)
+        e1.record(s)
+        capi.tttstate_step_done(eng.pool, g)
+        torch.cuda.synchronize()
+        read_ms.append(e0.elapsed_time(e1) / L)
+    read_ms = sorted(read_ms[2:])
+    read_bytes = (1 + B) * dm * dff * 2 + B * (dff + dm) * 2 * 2 + B * dm * 2
+    med = read_ms[len(read_ms) // 2]
+    res["read"] = {"ms_per_layer_median": med, "ms_min": read_ms[0], "GBps": read_bytes / med / 1e6,
+                   "frac_hbm": read_bytes / med / 1e6 / hbm, "alg_bytes": read_bytes}
+    # finish the chunk with READs (untimed) so the next step is a WRITE
+    while capi.tttstate_tail_len(eng.pool, owners[0]) < C - 1:
+        for l in range(L):
+            capi.read_apply(eng.pool, g, l, X[l], None, Vt[l], None, Y[l], None, None, s)
+        capi.tttstate_step_done(eng.pool, g)
+    for l in range(L):
+        capi.read_apply(eng.pool, gw, l, X[l], None, Vt[l], None, Y[l], None, None, s)
+    capi.tttstate_set_write_impl(a.write_impl)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    capi.write_commit(eng.pool, gw, 0.01, None, s)
+    e1.record(s)
+    torch.cuda.synchronize()
+    wms = e0.elapsed_time(e1) / L
+    wbytes = B * (2 * dm * dff * 2 + C * (dff + dm) * 2)
+    res["write"] = {"ms_per_layer": wms, "GBps": wbytes / wms / 1e6, "frac_hbm": wbytes / wms / 1e6 / hbm,
+                    "alg_bytes": wbytes, "impl": a.write_impl}
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
