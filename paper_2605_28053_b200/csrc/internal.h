@@ -57,6 +57,7 @@ struct CommitParams {
 
 int device_sm_count();
 cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s);
+bool read_decode_fits(int n, int d_model, int d_ff, int esize);
 cudaError_t launch_write_simt(int dtype, const WriteParams &p, cudaStream_t s);
 cudaError_t launch_write_tc(const WriteParams &p, cudaStream_t s);   // bf16, tcgen05
 bool write_tc_supported(int d_model, int d_ff, int C);

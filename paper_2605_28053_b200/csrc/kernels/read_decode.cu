@@ -5,19 +5,28 @@
 // P:403-409).  BASELINE.json north_star: y = x·(W_down + ΔW_owner)ᵀ.
 //
 // B200 design (DESIGN.md §"READ kernel"): decode READ is a set of GEMVs with
-// arithmetic intensity ≈ 2 flop/byte, i.e. HBM-bound by two
-// orders of magnitude, so it is a streaming SIMT kernel, not a tensor-core
-// GEMM.  One persistent CTA per SM (148 on B200) stages every member's x row
-// in shared memory once; warps stream whole 19 KB rows of W_down (read once
-// per group) and of each owner's ΔW (read once) with 16-byte
-// L1-no-allocate loads, 8 in flight per lane, and FMA in fp32.  A task is
-// (matrix m ∈ {base, member 0..n-1}, output row i); each task stores one fp32
-// partial, and the last of the n+1 tasks of row i (per-row ticket) sums
-// base + delta in a fixed order and writes y (deterministic; no atomics on
-// data).  The committed slot is selected through the device active-slot
-// table, so a commit enqueued earlier on the stream is visible without a
-// host round trip.
+// arithmetic intensity ≈ 2 flop/byte — HBM-bound by two orders of
+// magnitude — so it is a streaming SIMT kernel, not a tensor-core GEMM.  Its
+// speed is set by bytes in flight and by issue slots (tools/bw_probe.cu: a
+// pure 16-byte-load stream reaches ~6.8 TB/s with ≥ 64-128 KB in flight per
+// SM; a one-thread TMA bulk-copy ring tops out near 4.8 TB/s):
+//  * one persistent CTA per SM (148 on B200), 16 warps; every member's x row
+//    is staged in shared memory once per CTA;
+//  * a task is (matrix m ∈ {W_down, ΔW of member 0..n-1}, output row i); a
+//    warp streams the 19 KB row with 16-byte L1-no-allocate loads and keeps
+//    the next batch of 8 loads per lane (possibly of its next task) in flight
+//    while it consumes the current one;
+//  * bf16 products accumulate in fp32 with the mixed-precision FMA
+//    `fma.rn.f32.bf16` (SASS FHFMA.BF16 with .H0/.H1 half selects), so a
+//    16-byte vector costs 8 FMAs and no unpacking; fp32 uses FFMA2 pairs;
+//  * each task stores one fp32 partial; the last of the n+1 tasks of row i
+//    (per-row ticket) sums base + delta in a fixed order and writes y, so the
+//    result is deterministic and no data goes through atomics.
+// The committed slot is selected through the device active-slot table, so a
+// commit enqueued earlier on the stream is visible without a host round trip.
 #include <cuda_bf16.h>
+
+#include <algorithm>
 
 #include "../internal.h"
 
@@ -25,7 +34,10 @@ namespace ttt {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kUnroll = 8;
+constexpr int kWarps = kThreads / 32;
+constexpr int kU = 8;                       // 16-byte vectors per lane per batch
+
+typedef unsigned long long u64;
 
 __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
   uint4 r;
@@ -35,29 +47,50 @@ __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
   return r;
 }
 
-__device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
-__device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+// acc += w.lo*x.lo + w.hi*x.hi for one packed bf16 pair (fp32 accumulate)
+__device__ __forceinline__ void fma_bf16x2(float &acc, uint32_t w, uint32_t x) {
+  asm("{\n\t.reg .b16 wl, wh, xl, xh;\n\t"
+      "mov.b32 {wl, wh}, %1;\n\tmov.b32 {xl, xh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, wl, xl, %0;\n\tfma.rn.f32.bf16 %0, wh, xh, %0;\n}"
+      : "+f"(acc)
+      : "r"(w), "r"(x));
+}
+__device__ __forceinline__ u64 pack2(uint32_t lo, uint32_t hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ void ffma2(u64 &acc, u64 a, u64 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ float hsum2(u64 v) {
+  uint32_t lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+  return __uint_as_float(lo) + __uint_as_float(hi);
+}
 
-template <typename T>
-struct Elem;
-template <>
-struct Elem<__nv_bfloat16> {
+// Per element type: accumulator, 16-byte-vector dot, finish, conversions.
+template <typename T> struct Elem;
+template <> struct Elem<__nv_bfloat16> {
   static constexpr int kVec = 8;
-  // w (8 bf16) · x (8 bf16) accumulated into acc in element order
-  __device__ static __forceinline__ void unpack(const uint4 &v, float (&f)[8]) {
-    f[0] = bf_lo(v.x); f[1] = bf_hi(v.x); f[2] = bf_lo(v.y); f[3] = bf_hi(v.y);
-    f[4] = bf_lo(v.z); f[5] = bf_hi(v.z); f[6] = bf_lo(v.w); f[7] = bf_hi(v.w);
+  typedef float Acc;
+  __device__ static __forceinline__ Acc zero() { return 0.f; }
+  __device__ static __forceinline__ void dot(Acc &a, const uint4 &w, const uint4 &x) {
+    fma_bf16x2(a, w.x, x.x); fma_bf16x2(a, w.y, x.y); fma_bf16x2(a, w.z, x.z); fma_bf16x2(a, w.w, x.w);
   }
+  __device__ static __forceinline__ float finish(Acc a) { return a; }
   __device__ static __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
   __device__ static __forceinline__ __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
 };
-template <>
-struct Elem<float> {
+template <> struct Elem<float> {
   static constexpr int kVec = 4;
-  __device__ static __forceinline__ void unpack(const uint4 &v, float (&f)[4]) {
-    f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
-    f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+  typedef u64 Acc;
+  __device__ static __forceinline__ Acc zero() { return 0ull; }
+  __device__ static __forceinline__ void dot(Acc &a, const uint4 &w, const uint4 &x) {
+    ffma2(a, pack2(w.x, w.y), pack2(x.x, x.y));
+    ffma2(a, pack2(w.z, w.w), pack2(x.z, x.w));
   }
+  __device__ static __forceinline__ float finish(Acc a) { return hsum2(a); }
   __device__ static __forceinline__ float to_f(float v) { return v; }
   __device__ static __forceinline__ float from_f(float v) { return v; }
 };
@@ -65,15 +98,25 @@ struct Elem<float> {
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadParams p) {
   using E = Elem<T>;
-  constexpr int VN = E::kVec;
+  using Acc = typename E::Acc;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint4 *xs = reinterpret_cast<uint4 *>(smem_raw);   // [n][nvec] member x rows
+  uint4 *xs = reinterpret_cast<uint4 *>(smem_raw);      // [n][nvec] member x rows
+  __shared__ const uint4 *s_row0[kMaxReadMembers + 1];  // row-0 base of each matrix
 
   const int n = p.n, dff = p.d_ff, dm = p.d_model;
-  const int nvec = dff / VN;
+  const int nvec = dff / E::kVec;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // stage x rows (coalesced, once per CTA)
+  if (tid <= n) {
+    if (tid == 0) {
+      s_row0[0] = static_cast<const uint4 *>(p.w_down_l);
+    } else {
+      const int o = p.owner_idx[tid - 1];
+      const long long slot = 2LL * o + p.sel[o];
+      s_row0[tid] = reinterpret_cast<const uint4 *>(static_cast<const T *>(p.slots) + slot * p.slot_elems +
+                                                    p.layer_off);
+    }
+  }
   for (int idx = tid; idx < n * nvec; idx += kThreads) {
     const int b = idx / nvec, v = idx - b * nvec;
     xs[idx] = reinterpret_cast<const uint4 *>(static_cast<const T *>(p.X) + (size_t)p.x_row[b] * dff)[v];
@@ -91,114 +134,130 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
     for (int i = tid; i < dm; i += kThreads) tv[i] = src[i];
   }
 
-  const long long n_tasks = (long long)(n + 1) * dm;
-  const int warps_total = gridDim.x * (kThreads / 32);
-  const int gw = blockIdx.x * (kThreads / 32) + warp;
-  const int arrivals = n + 1;
+  const int n_tasks = (n + 1) * dm;
+  const int stride = gridDim.x * kWarps;
+  int t = blockIdx.x * kWarps + warp;
+  if (t >= n_tasks) return;
 
-  for (long long t = gw; t < n_tasks; t += warps_total) {
-    const int m = (int)(t / dm);          // 0 = base W_down, 1+b = member b's ΔW
-    const int i = (int)(t - (long long)m * dm);
-    const uint4 *row;
-    int b = 0;
-    if (m == 0) {
-      row = reinterpret_cast<const uint4 *>(static_cast<const T *>(p.w_down_l) + (size_t)i * dff);
-    } else {
-      b = m - 1;
-      const int o = p.owner_idx[b];
-      const long long slot = 2LL * o + p.sel[o];
-      row = reinterpret_cast<const uint4 *>(static_cast<const T *>(p.slots) + slot * p.slot_elems +
-                                            p.layer_off + (size_t)i * dff);
+  auto row_of = [&](int task) {
+    const int m = task / dm;
+    return s_row0[m] + (size_t)(task - m * dm) * nvec;
+  };
+  auto load = [&](uint4 (&buf)[kU], const uint4 *row, int v0) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (v0 + 32 * u < nvec) buf[u] = ld_stream(row + v0 + 32 * u);
+  };
+
+  uint4 cur[kU], nxt[kU];
+  const uint4 *row = row_of(t);
+  int v = lane;
+  load(cur, row, v);
+  Acc acc[kMaxReadMembers];
+#pragma unroll
+  for (int r = 0; r < kMaxReadMembers; ++r) acc[r] = E::zero();
+
+  while (true) {
+    // next batch: same row, or the first batch of this warp's next task
+    int nv = v + 32 * kU, nt = t;
+    const uint4 *nrow = row;
+    const bool task_end = nv >= nvec;
+    if (task_end) {
+      nt = t + stride;
+      nv = lane;
+      if (nt < n_tasks) nrow = row_of(nt);
     }
-    float acc[kMaxReadMembers];
-#pragma unroll
-    for (int r = 0; r < kMaxReadMembers; ++r) acc[r] = 0.f;
+    const bool more = nt < n_tasks;
+    if (more) load(nxt, nrow, nv);
 
-    for (int v0 = lane; v0 < nvec; v0 += 32 * kUnroll) {
-      uint4 w[kUnroll];
+    const int m = t / dm;
+    if (m == 0) {                                  // base W_down: every member's x
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (v0 + 32 * u < nvec) w[u] = ld_stream(row + v0 + 32 * u);
+      for (int u = 0; u < kU; ++u) {
+        if (v + 32 * u < nvec) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int v = v0 + 32 * u;
-        if (v < nvec) {
-          float wf[VN];
-          E::unpack(w[u], wf);
-          if (m == 0) {
+          for (int r = 0; r < kMaxReadMembers; ++r)
+            if (r < n) E::dot(acc[r], cur[u], xs[r * nvec + v + 32 * u]);
+        }
+      }
+    } else {                                       // member b's ΔW: its own x only
+      const uint4 *xb = xs + (m - 1) * nvec;
 #pragma unroll
-            for (int r = 0; r < kMaxReadMembers; ++r) {
-              if (r < n) {
-                float xf[VN];
-                E::unpack(xs[r * nvec + v], xf);
+      for (int u = 0; u < kU; ++u)
+        if (v + 32 * u < nvec) E::dot(acc[0], cur[u], xb[v + 32 * u]);
+    }
+
+    if (task_end) {
+      const int i = t - m * dm;
+      if (m == 0) {
+        float mine = 0.f;
 #pragma unroll
-                for (int e = 0; e < VN; ++e) acc[r] = fmaf(wf[e], xf[e], acc[r]);
-              }
-            }
-          } else {
-            float xf[VN];
-            E::unpack(xs[b * nvec + v], xf);
+        for (int r = 0; r < kMaxReadMembers; ++r) {
+          if (r < n) {
+            float s = E::finish(acc[r]);
 #pragma unroll
-            for (int e = 0; e < VN; ++e) acc[0] = fmaf(wf[e], xf[e], acc[0]);
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            mine = (lane == r) ? s : mine;
           }
+          acc[r] = E::zero();
         }
+        if (lane < n) p.Pbase[(size_t)lane * dm + i] = mine;
+      } else {
+        float s = E::finish(acc[0]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        acc[0] = E::zero();
+        if (lane == 0) p.Pdelta[(size_t)(m - 1) * dm + i] = s;
       }
-    }
-    // warp all-reduce (butterfly: every lane ends with the same sums)
-    if (m == 0) {
-#pragma unroll
-      for (int r = 0; r < kMaxReadMembers; ++r) {
-        if (r < n) {
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
+      __syncwarp();
+      int old = 0;
+      if (lane == 0) {
+        __threadfence();
+        old = atomicAdd(p.tickets + i, 1);
+      }
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (old == n) {                              // last of the n+1 arrivals for row i
+        __threadfence();
+        if (lane < n) {
+          float y = __ldcg(p.Pbase + (size_t)lane * dm + i) + __ldcg(p.Pdelta + (size_t)lane * dm + i);
+          if (p.resid) y += E::to_f(static_cast<const T *>(p.resid)[(size_t)p.y_row[lane] * dm + i]);
+          static_cast<T *>(p.Y)[(size_t)p.y_row[lane] * dm + i] = E::from_f(y);
         }
+        if (lane == 0) p.tickets[i] = 0;           // self-reset for the next launch
       }
-      // lane r stores member r's partial (static index select keeps acc in registers)
-      float mine = 0.f;
+    }
+    if (!more) break;
 #pragma unroll
-      for (int r = 0; r < kMaxReadMembers; ++r) mine = (lane == r) ? acc[r] : mine;
-      if (lane < n) p.Pbase[(size_t)lane * dm + i] = mine;
-    } else {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
-      if (lane == 0) p.Pdelta[(size_t)b * dm + i] = acc[0];
-    }
-    __syncwarp();
-    int old = 0;
-    if (lane == 0) {
-      __threadfence();
-      old = atomicAdd(p.tickets + i, 1);
-    }
-    old = __shfl_sync(0xffffffffu, old, 0);
-    if (old == arrivals - 1) {            // last arrival for row i: combine in fixed order
-      __threadfence();
-      if (lane < n) {
-        float y = __ldcg(p.Pbase + (size_t)lane * dm + i) + __ldcg(p.Pdelta + (size_t)lane * dm + i);
-        if (p.resid) y += E::to_f(static_cast<const T *>(p.resid)[(size_t)p.y_row[lane] * dm + i]);
-        static_cast<T *>(p.Y)[(size_t)p.y_row[lane] * dm + i] = E::from_f(y);
-      }
-      if (lane == 0) p.tickets[i] = 0;    // self-reset for the next launch
-    }
+    for (int u = 0; u < kU; ++u) cur[u] = nxt[u];
+    v = nv;
+    row = nrow;
+    t = nt;
   }
 }
 
+size_t smem_bytes(int n, int d_ff, int esize) { return (size_t)n * d_ff * esize; }
+
 template <typename T>
 cudaError_t launch_t(const ReadParams &p, cudaStream_t s) {
-  const size_t smem = (size_t)p.n * p.d_ff * sizeof(T);
-  static int configured_smem = -1;
-  if ((int)smem > configured_smem) {
+  const size_t smem = smem_bytes(p.n, p.d_ff, sizeof(T));
+  static int configured = -1;
+  if ((int)smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(read_decode_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return e;
-    configured_smem = (int)smem;
+    configured = (int)smem;
   }
-  const int grid = device_sm_count();
-  read_decode_kernel<T><<<grid, kThreads, smem, s>>>(p);
+  read_decode_kernel<T><<<device_sm_count(), kThreads, smem, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }
 
 }  // namespace
+
+bool read_decode_fits(int n, int d_model, int d_ff, int esize) {
+  (void)d_model;
+  return smem_bytes(n, d_ff, esize) <= 220 * 1024;
+}
 
 cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s) {
   if (dtype == 1) return launch_t<__nv_bfloat16>(p, s);

@@ -336,8 +336,10 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
   if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
   if (!X || !Vt || !Y) return fail(TTT_E_INVALID_ARG, "null X/Vt/Y");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int per = std::max(1, std::min(kMaxReadMembers, (int)((200 * 1024) / ((size_t)sh.d_ff * p->esize))));
-  if ((size_t)sh.d_ff * p->esize > 200 * 1024) return fail(TTT_E_SHAPE, "d_ff row exceeds shared memory");
+  int per = std::min(kMaxReadMembers, g->n);
+  while (per > 1 && !read_decode_fits(per, sh.d_model, sh.d_ff, (int)p->esize)) --per;
+  if (!read_decode_fits(per, sh.d_model, sh.d_ff, (int)p->esize))
+    return fail(TTT_E_SHAPE, "d_ff row slices exceed shared memory");
   for (int b0 = 0; b0 < g->n; b0 += per) {
     ReadParams rp{};
     rp.X = X; rp.Vt = Vt; rp.resid = resid; rp.Y = Y;

@@ -84,81 +84,132 @@ class InputSource:
         pass
 
 
-def run_trace(eng: Engine, tr, src: InputSource, stream=None, sync_writes: bool = True,
-              max_clock: int | None = None) -> RunLog:
-    """Alg. 1 over a workload.traces.Trace (App. H: fallback + wait budget)."""
-    log = RunLog()
-    owners = [tr.owner(s) for s in range(tr.n_streams)]
-    by_owner = {o: s for s, o in enumerate(owners)}
-    for s, o in enumerate(owners):
-        capi.tttstate_alloc(eng.pool, o, src.init_delta(s), tr.v0, stream)
-        pre = src.tail_prefill(s)
-        if pre is not None:
-            capi.tttstate_tail_load(eng.pool, o, pre[0], pre[1], pre[2], stream)
-    pos = [0] * tr.n_streams
-    pending: set = set()
-    ready_at: dict = {}
-    failed_once: set = set()
-    clock = 0
-    while any(p < tr.n_steps for p in pos):
-        if max_clock is not None and clock >= max_clock:
-            break
+class Server:
+    """Alg. 1 state for one trace: per-stream position, pending events, logs.
+
+    `step()` runs exactly one iteration of the serving loop at the current
+    clock.  With `profile=True` every read_apply / write_commit is bracketed by
+    CUDA events on `stream` (used by bench.py for the live per-kernel roofline).
+    """
+
+    def __init__(self, eng: Engine, tr, src: InputSource, stream=None, sync_writes: bool = True,
+                 profile: bool = False, profile_every: int = 1):
+        self.eng, self.tr, self.src, self.stream = eng, tr, src, stream
+        self.sync_writes, self.profile, self.profile_every = sync_writes, profile, max(1, profile_every)
+        self.log = RunLog()
+        self.owners = [tr.owner(s) for s in range(tr.n_streams)]
+        self.by_owner = {o: s for s, o in enumerate(self.owners)}
+        self.pos = [0] * tr.n_streams
+        self.pending: set = set()
+        self.ready_at: dict = {}
+        self.failed_once: set = set()
+        self.clock = 0
+        self.read_events: list = []       # (start, end) CUDA event pairs around read_apply
+        self.write_events: list = []      # (start, end) around write_commit
+
+    def admit(self):
+        eng, tr, src = self.eng, self.tr, self.src
+        for s, o in enumerate(self.owners):
+            capi.tttstate_alloc(eng.pool, o, src.init_delta(s), tr.v0, self.stream)
+            pre = src.tail_prefill(s)
+            if pre is not None:
+                capi.tttstate_tail_load(eng.pool, o, pre[0], pre[1], pre[2], self.stream)
+
+    def done(self) -> bool:
+        return all(p >= self.tr.n_steps for p in self.pos)
+
+    def _ev(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream() if self.stream is None else self.stream)
+        return e
+
+    def step(self):
+        eng, tr, src, log, stream = self.eng, self.tr, self.src, self.log, self.stream
+        pool, owners, clock = eng.pool, self.owners, self.clock
         events = []
         for s in range(tr.n_streams):                                   # View + NextStep
-            if pos[s] < tr.n_steps and s not in pending:
-                for op in tr.controls_at(s, pos[s]):
+            if self.pos[s] < tr.n_steps and s not in self.pending:
+                for op in tr.controls_at(s, self.pos[s]):
                     if op == "snapshot":
-                        capi.tttstate_snapshot(eng.pool, owners[s], stream)
+                        capi.tttstate_snapshot(pool, owners[s], stream)
                     elif op == "rollback":
-                        vb = capi.tttstate_version(eng.pool, owners[s])
-                        va = capi.rollback(eng.pool, owners[s], stream)
-                        log.commits.append((s, pos[s], vb, va, "rolled_back"))
-                events.append(capi.tttstate_next_event(eng.pool, owners[s], clock))
-                pending.add(s)
-                ready_at[s] = clock
+                        vb = capi.tttstate_version(pool, owners[s])
+                        va = capi.rollback(pool, owners[s], stream)
+                        log.commits.append((s, self.pos[s], vb, va, "rolled_back"))
+                events.append(capi.tttstate_next_event(pool, owners[s], clock))
+                self.pending.add(s)
+                self.ready_at[s] = clock
         groups, rejected = capi.plan_batch(eng.planner, events, clock)  # LegalGroups
         if rejected:
             raise RuntimeError(f"planner rejected events of a well-formed trace: {rejected}")
         for g in groups:
-            ss = [by_owner[o] for o in g.owners]
-            ps = [pos[s] for s in ss]
-            log.plan.append((g.issue_step, g.effect, ss, [ready_at[s] for s in ss]))
+            ss = [self.by_owner[o] for o in g.owners]
+            ps = [self.pos[s] for s in ss]
+            log.plan.append((g.issue_step, g.effect, ss, [self.ready_at[s] for s in ss]))
+            prof = self.profile and clock % self.profile_every == 0
             for l in range(tr.n_layers):                                # ExecuteOperatorGroup
                 X, xr, Vt, vr, Y, yr = src.group_io(l, ss, ps)
-                capi.read_apply(eng.pool, g, l, X, xr, Vt, vr, Y, yr, None, stream)
+                if prof:
+                    e0 = self._ev()
+                capi.read_apply(pool, g, l, X, xr, Vt, vr, Y, yr, None, stream)
+                if prof:
+                    self.read_events.append((e0, self._ev()))
                 src.on_output(l, ss, ps, Y, yr)                         # ReturnOutputs
             log.census[g.effect] += len(ss)
             if g.effect == READ:
-                capi.tttstate_step_done(eng.pool, g)                    # UpdateKVAndTailMetadata
+                capi.tttstate_step_done(pool, g)                        # UpdateKVAndTailMetadata
             else:
-                vb = [capi.tttstate_version(eng.pool, o) for o in g.owners]
-                mask = [("fail" in tr.controls_at(s, p)) and (s, p) not in failed_once for s, p in zip(ss, ps)]
-                try:                                                    # CommitVersions
-                    capi.write_commit(eng.pool, g, tr.eta, mask if any(mask) else None, stream)
-                    ok = True
-                    if sync_writes and capi.tttstate_sync(eng.pool, stream):
-                        log.device_failures += 1
-                        ok = False
-                except TTTError as e:
-                    if e.status != capi.TTT_E_WRITE_FAILED:
-                        raise
-                    ok = False
-                if ok:
-                    for s, p, v in zip(ss, ps, vb):
-                        log.commits.append((s, p, v, v + 1, "ok"))
-                else:
-                    for s, p, v in zip(ss, ps, vb):
-                        failed_once.add((s, p))
-                        log.commits.append((s, p, v, v, "failed"))
-                    log.fallbacks += 1
-                    for s, p, v, o in zip(ss, ps, vb, g.owners):        # App. H fallback: singletons
-                        single = Group(WRITE, [o], g.c.shape_id, g.c.placement, g.c.backend, clock)
-                        capi.write_commit(eng.pool, single, tr.eta, None, stream)
-                        log.commits.append((s, p, v, v + 1, "ok"))
+                self._write(g, ss, ps)
             for s in ss:
-                pos[s] += 1
-                pending.discard(s)
-        clock += 1
-    for s, o in enumerate(owners):
-        log.versions[s] = capi.tttstate_version(eng.pool, o)
-    return log
+                self.pos[s] += 1
+                self.pending.discard(s)
+        self.clock += 1
+
+    def _write(self, g, ss, ps):
+        eng, tr, log, stream = self.eng, self.tr, self.log, self.stream
+        pool = eng.pool
+        vb = [capi.tttstate_version(pool, o) for o in g.owners]
+        mask = [("fail" in tr.controls_at(s, p)) and (s, p) not in self.failed_once for s, p in zip(ss, ps)]
+        try:                                                            # CommitVersions
+            if self.profile:
+                e0 = self._ev()
+            capi.write_commit(pool, g, tr.eta, mask if any(mask) else None, stream)
+            if self.profile:
+                self.write_events.append((e0, self._ev()))
+            ok = True
+            if self.sync_writes and capi.tttstate_sync(pool, stream):
+                log.device_failures += 1
+                ok = False
+        except TTTError as e:
+            if e.status != capi.TTT_E_WRITE_FAILED:
+                raise
+            ok = False
+        if ok:
+            for s, p, v in zip(ss, ps, vb):
+                log.commits.append((s, p, v, v + 1, "ok"))
+            return
+        for s, p, v in zip(ss, ps, vb):
+            self.failed_once.add((s, p))
+            log.commits.append((s, p, v, v, "failed"))
+        log.fallbacks += 1
+        for s, p, v, o in zip(ss, ps, vb, g.owners):                    # App. H fallback: singletons
+            single = Group(WRITE, [o], g.c.shape_id, g.c.placement, g.c.backend, self.clock)
+            capi.write_commit(pool, single, tr.eta, None, stream)
+            log.commits.append((s, p, v, v + 1, "ok"))
+
+    def finish(self) -> RunLog:
+        for s, o in enumerate(self.owners):
+            self.log.versions[s] = capi.tttstate_version(self.eng.pool, o)
+        return self.log
+
+
+def run_trace(eng: Engine, tr, src: InputSource, stream=None, sync_writes: bool = True,
+              max_clock: int | None = None) -> RunLog:
+    """Alg. 1 over a workload.traces.Trace (App. H: fallback + wait budget)."""
+    srv = Server(eng, tr, src, stream, sync_writes)
+    srv.admit()
+    while not srv.done():
+        if max_clock is not None and srv.clock >= max_clock:
+            break
+        srv.step()
+    return srv.finish()
