@@ -33,9 +33,9 @@
 namespace ttt {
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
-constexpr int kU = 8;                       // 16-byte vectors per lane per batch
+constexpr int kU = 4;                       // 16-byte vectors per lane per batch
 
 typedef unsigned long long u64;
 
@@ -183,8 +183,8 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
     } else {                                       // member b's ΔW: its own x only
       const uint4 *xb = xs + (m - 1) * nvec;
 #pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (v + 32 * u < nvec) E::dot(acc[0], cur[u], xb[v + 32 * u]);
+      for (int u = 0; u < kU; ++u)                 // kU independent FMA chains
+        if (v + 32 * u < nvec) E::dot(acc[u % kMaxReadMembers], cur[u], xb[v + 32 * u]);
     }
 
     if (task_end) {
@@ -205,8 +205,11 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
       } else {
         float s = E::finish(acc[0]);
 #pragma unroll
+        for (int r = 1; r < kMaxReadMembers; ++r) s += E::finish(acc[r]);
+#pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        acc[0] = E::zero();
+#pragma unroll
+        for (int r = 0; r < kMaxReadMembers; ++r) acc[r] = E::zero();
         if (lane == 0) p.Pdelta[(size_t)(m - 1) * dm + i] = s;
       }
       __syncwarp();
