@@ -41,6 +41,7 @@ struct WriteParams {
   float eta;
   int *fail_flag;
   int n, d_model, d_ff, C;
+  int max_owners, max_slots;     // tensor-map extents (tails, pool slots)
   int owner_idx[kMaxGroup];
 };
 

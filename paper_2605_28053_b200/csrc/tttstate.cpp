@@ -434,6 +434,7 @@ ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32
   wp.eta = eta;
   wp.fail_flag = p->d_fail_flag();
   wp.n = g->n; wp.d_model = sh.d_model; wp.d_ff = sh.d_ff; wp.C = sh.chunk;
+  wp.max_owners = p->max_owners; wp.max_slots = 2 * p->max_owners + p->n_ckpt;
   for (int b = 0; b < g->n; ++b) wp.owner_idx[b] = recs[b]->idx;
   const int impl = g_write_impl.load();
   const bool use_tc = sh.dtype == TTT_BF16 && impl != 1 && write_tc_supported(sh.d_model, sh.d_ff, sh.chunk);
