@@ -347,7 +347,8 @@ def main():
                       "achieved_GBps": (write_bytes / (write_avg / 1e3) / 1e9) if write_avg else None,
                       "frac": (write_bytes / (write_avg / 1e3) / 1e9 / hbm) if write_avg else None,
                       "alg_bytes_per_call": write_bytes},
-            "read_share_of_step": sum(read_ms) / ms,
+            # READ launches per timed window: L per decode step; events sample 1 step in 8
+            "read_share_of_step": read_avg * L * window * a.steps / ms,
             "clocks": clk.summary(),
         }
         if world == 1 and not a.no_cpu_baseline:

@@ -39,9 +39,11 @@ namespace ttt {
 namespace {
 
 constexpr int BM = 128, BN = 128;
-constexpr int kEpiThreads = 128;
-constexpr int kThreads = 64 + kEpiThreads;      // producer warp, MMA warp, 4 epilogue warps
+constexpr int kEpiThreads = 256;                 // 8 epilogue warps: 2 per TMEM lane quarter
+constexpr int kThreads = 64 + kEpiThreads;      // producer warp, MMA warp, 8 epilogue warps
 constexpr int kTmemCols = 2 * BN;                 // two fp32 accumulators of 128 columns
+constexpr int kBox = BM * 128;                    // one 128-row x 64-column bf16 box (16 KB)
+constexpr int kSB = 7;                            // committed-ΔW box ring depth (3.5 tiles ahead)
 
 typedef unsigned long long u64;
 
@@ -129,6 +131,24 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ u64 pack_u2(uint32_t lo, uint32_t hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ u64 pack_f2(float lo, float hi) { return pack_u2(__float_as_uint(lo), __float_as_uint(hi)); }
+// v = a*b + v on fp32 pairs (FFMA2)
+__device__ __forceinline__ void ffma2(u64 &v, u64 a, u64 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(v) : "l"(a), "l"(b));
+}
+// fp32 pair -> packed bf16x2 (low half = first element), round to nearest even
+__device__ __forceinline__ uint32_t cvt_bf16x2(u64 v) {
+  uint32_t lo, hi, r;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(hi)), "f"(__uint_as_float(lo)));
+  return r;
+}
+
 struct Tile {
   int b, jb, ib;
 };
@@ -140,14 +160,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 1024-byte aligned carve-up: A ring [2][C x 128], B [C x 128], S (ΔW tile) ring [2][128 x 128]
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int C = p.C;
-  const uint32_t a_bytes = (uint32_t)C * BM * 2, b_bytes = (uint32_t)C * BN * 2, s_bytes = BM * BN * 2;
+  const uint32_t a_bytes = (uint32_t)C * BM * 2, b_bytes = (uint32_t)C * BN * 2;
   unsigned char *sA = smem;                       // 2 stages
   unsigned char *sB = sA + 2 * a_bytes;
-  unsigned char *sS = sB + b_bytes;               // 2 stages
-  u64 *bars = reinterpret_cast<u64 *>(sS + 2 * s_bytes);
+  unsigned char *sS = sB + b_bytes;               // kSB boxes of 16 KB
+  u64 *bars = reinterpret_cast<u64 *>(sS + kSB * kBox);
   u64 *a_full = bars, *a_empty = bars + 2, *b_full = bars + 4, *b_empty = bars + 5;
-  u64 *s_full = bars + 6, *s_empty = bars + 8, *t_full = bars + 10, *t_empty = bars + 12;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 14);
+  u64 *t_full = bars + 6, *t_empty = bars + 8, *s_full = bars + 10, *s_empty = bars + 10 + kSB;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 10 + 2 * kSB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mb = p.d_model / BM, nb = p.d_ff / BN;
@@ -168,10 +188,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(a_full + s, 1);
       mbar_init(a_empty + s, 1);
-      mbar_init(s_full + s, 1);
-      mbar_init(s_empty + s, 1);
       mbar_init(t_full + s, 1);
       mbar_init(t_empty + s, kEpiThreads / 32);
+    }
+    for (int s = 0; s < kSB; ++s) {
+      mbar_init(s_full + s, 1);
+      mbar_init(s_empty + s, 1);
     }
     mbar_init(b_full, 1);
     mbar_init(b_empty, 1);
@@ -193,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch(&tmV);
       tma_prefetch(&tmZ);
       tma_prefetch(&tmW);
-      int k = 0, strip = -1, nstrip = 0;
+      int k = 0, kb = 0, strip = -1, nstrip = 0;
       for (int t = t0; t < t1; ++t, ++k) {
         const Tile tl = tile_of(t);
         const int o = p.owner_idx[tl.b];
@@ -212,12 +234,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(a_full + s, a_bytes);
         for (int h = 0; h < BM / 64; ++h)
           tma_load_3d(sA + s * a_bytes + h * (C * 128), &tmV, a_full + s, tl.ib * BM + 64 * h, 0, tail_idx);
-        if (k >= 2) mbar_wait(s_empty + s, ((k >> 1) - 1) & 1);
-        mbar_expect_tx(s_full + s, s_bytes);
         const int src_slot = 2 * o + p.sel[o];
-        for (int h = 0; h < BN / 64; ++h)
-          tma_load_3d(sS + s * s_bytes + h * (BM * 128), &tmW, s_full + s, tl.jb * BN + 64 * h, tl.ib * BM,
-                      src_slot * p.L + p.layer);
+        for (int h = 0; h < BN / 64; ++h, ++kb) {
+          const int sb = kb % kSB;
+          if (kb >= kSB) mbar_wait(s_empty + sb, ((kb / kSB) - 1) & 1);
+          mbar_expect_tx(s_full + sb, kBox);
+          tma_load_3d(sS + sb * kBox, &tmW, s_full + sb, tl.jb * BN + 64 * h, tl.ib * BM, src_slot * p.L + p.layer);
+        }
       }
     }
   } else if (warp == 1) {
@@ -253,58 +276,61 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2-5)
+    // ------------------------------------------------------------ epilogue (warps 2-9)
     const int q = warp & 3;                       // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;             // which 32-column half of each 64-column box
     const int row = q * 32 + lane;                // output row within the tile
     const int et = threadIdx.x - 64;
-    bool bad = false;
-    int k = 0;
+    uint32_t expmax = 0;                          // max exponent field seen (non-finite guard)
+    const u64 eta2 = pack_f2(p.eta, p.eta);
+    int k = 0, kb = 0;
     for (int t = t0; t < t1; ++t, ++k) {
       const Tile tl = tile_of(t);
-      const int s = k & 1, acc = k & 1;
+      const int acc = k & 1;
       mbar_wait(t_full + acc, (k >> 1) & 1);
-      mbar_wait(s_full + s, (k >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      unsigned char *tileS = sS + s * s_bytes;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      const int o = p.owner_idx[tl.b];
+      const int dst_slot = 2 * o + 1 - p.sel[o];
+      for (int h = 0; h < BN / 64; ++h, ++kb) {
+        const int sb = kb % kSB;
         uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
-        // 32 columns = 4 16-byte chunks in box (c / 2), chunks (c % 2)*4 .. +3, 128B-swizzled by row
-        unsigned char *rowp = tileS + (c >> 1) * (BM * 128) + row * 128;
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + h * 64 + half * 32), r);
+        if (h == BN / 64 - 1) {                   // this warp has drained its part of the accumulator
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(t_empty + acc);
+        }
+        mbar_wait(s_full + sb, (kb / kSB) & 1);
+        unsigned char *rowp = sS + sb * kBox + row * 128;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int ch = ((c & 1) * 4 + u) ^ (row & 7);
+          const int ch = (half * 4 + u) ^ (row & 7);  // 128-byte swizzle: 16-byte chunk ^ (row % 8)
           uint4 *ptr = reinterpret_cast<uint4 *>(rowp + ch * 16);
           uint4 w = *ptr;
           uint32_t *wv = reinterpret_cast<uint32_t *>(&w);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float lo = __uint_as_float(wv[e] << 16), hi = __uint_as_float(wv[e] & 0xffff0000u);
-            const float a0 = __uint_as_float(r[u * 8 + 2 * e]), a1 = __uint_as_float(r[u * 8 + 2 * e + 1]);
-            __nv_bfloat162 o2 = __floats2bfloat162_rn(fmaf(p.eta, a0, lo), fmaf(p.eta, a1, hi));
-            const float2 back = __bfloat1622float2(o2);
-            bad |= !(isfinite(back.x) && isfinite(back.y));
-            wv[e] = *reinterpret_cast<uint32_t *>(&o2);
+            // (ΔW_v lo, hi) + η·(acc lo, hi) in fp32x2, one RNE pack to bf16x2
+            u64 a2 = pack_u2(r[u * 8 + 2 * e], r[u * 8 + 2 * e + 1]);
+            u64 v2 = pack_u2(wv[e] << 16, wv[e] & 0xffff0000u);
+            ffma2(v2, eta2, a2);
+            const uint32_t ob = cvt_bf16x2(v2);
+            expmax = __vmaxu2(expmax, ob & 0x7f807f80u);
+            wv[e] = ob;
           }
           *ptr = w;
         }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(t_empty + acc);  // accumulator may be overwritten
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // smem writes -> TMA store
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
-      if (et == 0) {
-        const int o = p.owner_idx[tl.b];
-        const int dst_slot = 2 * o + 1 - p.sel[o];
-        for (int h = 0; h < BN / 64; ++h)
-          tma_store_3d(&tmW, tileS + h * (BM * 128), tl.jb * BN + 64 * h, tl.ib * BM, dst_slot * p.L + p.layer);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   // store of tile k-1 has read its smem
-        if (k >= 1) mbar_arrive(s_empty + ((k - 1) & 1));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // smem writes -> TMA store
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+        if (et == 0) {
+          tma_store_3d(&tmW, sS + sb * kBox, tl.jb * BN + 64 * h, tl.ib * BM, dst_slot * p.L + p.layer);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");   // box kb-2 has been read out
+          if (kb >= 2) mbar_arrive(s_empty + (kb - 2) % kSB);
+        }
       }
     }
+    const bool bad = (expmax & 0x7f80u) == 0x7f80u || (expmax >> 16) == 0x7f80u;
     if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (bad) atomicOr(p.fail_flag, 1);
   }
@@ -339,7 +365,7 @@ bool make_map(CUtensorMap *m, void *base, uint64_t d0, uint64_t d1, uint64_t d2,
          CUDA_SUCCESS;
 }
 
-size_t smem_bytes(int C) { return 1024 + 2 * (size_t)C * BM * 2 + (size_t)C * BN * 2 + 2 * (size_t)BM * BN * 2 + 256; }
+size_t smem_bytes(int C) { return 1024 + 2 * (size_t)C * BM * 2 + (size_t)C * BN * 2 + (size_t)kSB * kBox + 512; }
 
 }  // namespace
 

@@ -79,16 +79,25 @@ def main():
         for l in range(L):
             capi.read_apply(eng.pool, g, l, X[l], None, Vt[l], None, Y[l], None, None, s)
         capi.tttstate_step_done(eng.pool, g)
-    for l in range(L):
-        capi.read_apply(eng.pool, gw, l, X[l], None, Vt[l], None, Y[l], None, None, s)
     capi.tttstate_set_write_impl(a.write_impl)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(s)
-    capi.write_commit(eng.pool, gw, 0.01, None, s)
-    e1.record(s)
-    torch.cuda.synchronize()
-    wms = e0.elapsed_time(e1) / L
+
+    def boundary(timed):
+        for l in range(L):
+            capi.read_apply(eng.pool, gw, l, X[l], None, Vt[l], None, Y[l], None, None, s)
+        # the stream is still busy with the READs: no host-side gap lands inside the timed region
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        capi.write_commit(eng.pool, gw, 0.01, None, s)
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    boundary(False)                                   # first call: attribute setup, map encode warm-up
+    for _ in range(C - 1):
+        for l in range(L):
+            capi.read_apply(eng.pool, g, l, X[l], None, Vt[l], None, Y[l], None, None, s)
+        capi.tttstate_step_done(eng.pool, g)
+    wms = boundary(True) / L
     wbytes = B * (2 * dm * dff * 2 + C * (dff + dm) * 2)
     res["write"] = {"ms_per_layer": wms, "GBps": wbytes / wms / 1e6, "frac_hbm": wbytes / wms / 1e6 / hbm,
                     "alg_bytes": wbytes, "impl": a.write_impl}
