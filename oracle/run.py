@@ -75,11 +75,12 @@ def _control(tab, tr, rec, s, p):
             rec.commits.append((s, p, v_before, v_after, "rolled_back"))
 
 
-def run_sequential(tr: Trace, layers=None, keep_outputs: bool = True) -> Record:
+def run_sequential(tr: Trace, layers=None, keep_outputs: bool = True, streams=None) -> Record:
+    """Sequential execution; `streams` restricts it to a subset (streams are independent)."""
     layers = list(range(tr.n_layers)) if layers is None else list(layers)
     tab = make_table(tr, layers)
     rec = Record()
-    for s in range(tr.n_streams):
+    for s in (range(tr.n_streams) if streams is None else streams):
         init_stream(tab, tr, s, layers)
         r = tr.owner(s)
         for p in range(tr.n_steps):

@@ -65,3 +65,57 @@ def make_engine(tr, device="cuda", n_ckpt=4, max_owners=None, mode=None, B=None,
                   max_owners or tr.n_streams + 2, W, n_ckpt=n_ckpt,
                   mode=tr.mode if mode is None else mode, B=tr.B if B is None else B,
                   w=tr.w if w is None else w, eta=tr.eta)
+
+
+class DeviceGenInputs(InputSource):
+    """Paper-sized inputs generated on the device by libttt_gen.so with the same counter
+    keys as workload/ (bit-identical: tests/test_gpu_parity.py::test_generator_device_matches_numpy)."""
+
+    def __init__(self, tr, device, record_streams=()):
+        from paper_2605_28053_b200 import capi
+        from workload import rng
+        self.capi, self.rng, self.tr, self.dev = capi, rng, tr, device
+        self.bf16 = tr.dtype == "bf16"
+        self.tdt = torch.bfloat16 if self.bf16 else torch.float32
+        self.record = set(record_streams)
+        self.out = {}
+
+    def _gen(self, shape, tensor, owner, layer, pos, amp):
+        t = torch.empty(*shape, dtype=self.tdt, device=self.dev)
+        self.capi.gen_uniform(t, self.tr.seed, tensor, owner, layer, pos, t.numel(), amp, self.bf16)
+        return t
+
+    def w_down(self):
+        tr, rng = self.tr, self.rng
+        return torch.stack([self._gen((tr.d_model, tr.d_ff), rng.T_W_DOWN, 0, l, 0, tr.amp_w)
+                            for l in range(tr.n_layers)])
+
+    def init_delta(self, s):
+        tr, rng = self.tr, self.rng
+        if tr.delta0 == "zero":
+            return None
+        return torch.stack([self._gen((tr.d_model, tr.d_ff), rng.T_DELTA0, tr.owner(s), l, 0, tr.amp_w)
+                            for l in range(tr.n_layers)])
+
+    def tail_prefill(self, s):
+        tr, rng = self.tr, self.rng
+        off = tr.offset(s)
+        if not off:
+            return None
+        Z = torch.stack([torch.stack([self._gen((tr.d_ff,), rng.T_X, tr.owner(s), l, p, 1.0) for p in range(-off, 0)])
+                         for l in range(tr.n_layers)])
+        V = torch.stack([torch.stack([self._gen((tr.d_model,), rng.T_TGT, tr.owner(s), l, p, 1.0)
+                                      for p in range(-off, 0)]) for l in range(tr.n_layers)])
+        return off, Z, V
+
+    def group_io(self, l, ss, ps):
+        tr, rng = self.tr, self.rng
+        X = torch.stack([self._gen((tr.d_ff,), rng.T_X, tr.owner(s), l, p, 1.0) for s, p in zip(ss, ps)])
+        Vt = torch.stack([self._gen((tr.d_model,), rng.T_TGT, tr.owner(s), l, p, 1.0) for s, p in zip(ss, ps)])
+        Y = torch.empty(len(ss), tr.d_model, dtype=self.tdt, device=self.dev)
+        return X, None, Vt, None, Y, None
+
+    def on_output(self, l, ss, ps, Y, yr):
+        for k, (s, p) in enumerate(zip(ss, ps)):
+            if s in self.record:
+                self.out[(s, p, l)] = to_host_f64(Y[k])
