@@ -27,15 +27,15 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "../internal.h"
 
 namespace ttt {
 namespace {
 
-constexpr int kThreads = 1024;
-constexpr int kWarps = kThreads / 32;
-constexpr int kU = 4;                       // 16-byte vectors per lane per batch
+// Launch variants (threads per CTA, 16-byte loads per lane per batch): the
+// default was chosen by a sweep (TTT_READ_CFG selects another for tuning).
 
 typedef unsigned long long u64;
 
@@ -95,8 +95,9 @@ template <> struct Elem<float> {
   __device__ static __forceinline__ float from_f(float v) { return v; }
 };
 
-template <typename T>
+template <typename T, int kThreads, int kU>
 __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadParams p) {
+  constexpr int kWarps = kThreads / 32;
   using E = Elem<T>;
   using Acc = typename E::Acc;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -240,19 +241,40 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
 
 size_t smem_bytes(int n, int d_ff, int esize) { return (size_t)n * d_ff * esize; }
 
-template <typename T>
-cudaError_t launch_t(const ReadParams &p, cudaStream_t s) {
+template <typename T, int TH, int U>
+cudaError_t launch_cfg(const ReadParams &p, cudaStream_t s) {
   const size_t smem = smem_bytes(p.n, p.d_ff, sizeof(T));
   static int configured = -1;
   if ((int)smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(read_decode_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(read_decode_kernel<T, TH, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return e;
     configured = (int)smem;
   }
-  read_decode_kernel<T><<<device_sm_count(), kThreads, smem, s>>>(p);
+  read_decode_kernel<T, TH, U><<<device_sm_count(), TH, smem, s>>>(p);
   count_launch();
   return cudaGetLastError();
+}
+
+int read_cfg() {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char *e = getenv("TTT_READ_CFG");
+    cfg = e ? atoi(e) : 0;
+  }
+  return cfg;
+}
+
+template <typename T>
+cudaError_t launch_t(const ReadParams &p, cudaStream_t s) {
+  switch (read_cfg()) {
+    case 1: return launch_cfg<T, 1024, 3>(p, s);
+    case 2: return launch_cfg<T, 1024, 2>(p, s);
+    case 3: return launch_cfg<T, 768, 5>(p, s);
+    case 4: return launch_cfg<T, 640, 6>(p, s);
+    case 5: return launch_cfg<T, 896, 4>(p, s);
+    default: return launch_cfg<T, 1024, 4>(p, s);
+  }
 }
 
 }  // namespace
