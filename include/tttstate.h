@@ -172,6 +172,19 @@ ttt_status read_apply(ttt_pool *pool, const ttt_group *g, int32_t layer, const v
                       const int32_t *x_rows, const void *Vt, const int32_t *v_rows, void *Y,
                       const int32_t *y_rows, const void *resid, void *stream);
 
+/* NEXT f2 — chunk-granular READ (prefill): for every member b of WRITE group g,
+ * whose tail is empty, apply all C tokens of its next chunk at the committed
+ * version v in one tensor-core GEMM per layer and append them to the tail:
+ *   Y[b, t, :] = X[b, t, :] · (W_down[layer] + ΔW_{μ(b)}[layer])ᵀ,  t < C
+ * X [n][C][d_ff], Vt [n][C][d_model], Y [n][C][d_model], device, bf16 only.
+ * After every layer was applied the chunk's boundary token counts as applied:
+ * call write_commit(g) to commit v+1 (same group).  Paper: READs of a chunk
+ * keep version v (Table 3); chunk boundaries every C_ttt tokens
+ * (P:160-161).  Errors: TTT_E_SHAPE (not bf16 / d_ff % 64 / d_model % 128 or
+ * 160 / C > 128), TTT_E_TAIL_FULL (not at a chunk start), TTT_E_ALREADY_APPLIED. */
+ttt_status read_apply_chunk(ttt_pool *pool, const ttt_group *g, int32_t layer, const void *X, const void *Vt,
+                            void *Y, void *stream);
+
 /* UpdateKVAndTailMetadata for a READ group once every layer was applied:
  * tail length += 1 per member (Alg. 1 line 13).                             */
 ttt_status tttstate_step_done(ttt_pool *pool, const ttt_group *g);

@@ -86,6 +86,7 @@ _sigs = {
     "read_apply": (C.c_int, [P, C.POINTER(ttt_group), C.c_int32, P, C.POINTER(C.c_int32), P,
                              C.POINTER(C.c_int32), P, C.POINTER(C.c_int32), P, P]),
     "tttstate_step_done": (C.c_int, [P, C.POINTER(ttt_group)]),
+    "read_apply_chunk": (C.c_int, [P, C.POINTER(ttt_group), C.c_int32, P, P, P, P]),
     "write_commit": (C.c_int, [P, C.POINTER(ttt_group), C.c_float, C.POINTER(C.c_uint32),
                                C.POINTER(C.c_uint64), P]),
     "tttstate_snapshot": (C.c_int, [P, C.c_uint64, P]),
@@ -268,6 +269,11 @@ def validate_group(pool, group: Group, expected_versions=None):
 def read_apply(pool, group: Group, layer: int, X, x_rows, Vt, v_rows, Y, y_rows=None, resid=None, stream=None):
     _check(_lib.read_apply(pool, C.byref(group.c), layer, _ptr(X), _rows(x_rows), _ptr(Vt), _rows(v_rows),
                            _ptr(Y), _rows(y_rows), _ptr(resid), _stream(stream)))
+
+
+def read_apply_chunk(pool, group: Group, layer: int, X, Vt, Y, stream=None):
+    """NEXT f2: all C tokens of each member's chunk at version v (tcgen05); then write_commit."""
+    _check(_lib.read_apply_chunk(pool, C.byref(group.c), layer, _ptr(X), _ptr(Vt), _ptr(Y), _stream(stream)))
 
 
 def tttstate_step_done(pool, group: Group):

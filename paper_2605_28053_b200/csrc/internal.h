@@ -56,7 +56,19 @@ struct CommitParams {
   int owner_idx[kMaxGroup];
 };
 
+// NEXT f2: chunk-granular READ of C tokens per member at one version (tcgen05).
+struct ChunkLaunch {
+  int n, d_model, d_ff, C, L, layer, max_slots;
+  const int *sel;
+  const void *X, *Vt, *w_down, *slots;
+  void *Y, *tailZ, *tailV;
+  long long tz_owner, tv_owner, tz_layer, tv_layer;
+  int owner_idx[kMaxGroup];
+};
+
 int device_sm_count();
+bool read_chunk_supported(int d_model, int d_ff, int C);
+cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s);
 cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s);
 bool read_decode_fits(int n, int d_model, int d_ff, int esize);
 cudaError_t launch_write_simt(int dtype, const WriteParams &p, cudaStream_t s);

@@ -19,6 +19,7 @@ struct OwnerRec {
   int tail_len = 0;           // completed tokens in the current chunk
   std::vector<uint8_t> applied;   // per layer: current token appended
   int n_applied = 0;
+  bool chunk_mode = false;    // current chunk applied by read_apply_chunk (f2)
   bool has_ckpt = false;      // c_r^v
   uint64_t ckpt_v = 0;
   int ckpt_sel = 0;           // pinned pair slot (when ckpt_pool < 0)

@@ -116,6 +116,7 @@ ttt_status check_group(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec *> 
 void clear_applied(OwnerRec &r) {
   std::fill(r.applied.begin(), r.applied.end(), 0);
   r.n_applied = 0;
+  r.chunk_mode = false;
 }
 
 }  // namespace
@@ -332,6 +333,7 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
       return fail(TTT_E_WRONG_EFFECT, "owner " + std::to_string(g->owner_map[b]) +
                                           (boundary ? " is at a chunk boundary (WRITE step)" : " is not at a boundary"));
     if (r.applied[layer]) return fail(TTT_E_ALREADY_APPLIED, "owner " + std::to_string(g->owner_map[b]));
+    if (r.chunk_mode) return fail(TTT_E_WRONG_EFFECT, "owner " + std::to_string(g->owner_map[b]) + " is mid-chunk");
   }
   if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
   if (!X || !Vt || !Y) return fail(TTT_E_INVALID_ARG, "null X/Vt/Y");
@@ -387,6 +389,49 @@ ttt_status tttstate_step_done(ttt_pool *p, const ttt_group *g) {
   for (int b = 0; b < g->n; ++b) {
     recs[b]->tail_len += 1;
     clear_applied(*recs[b]);
+  }
+  return TTT_OK;
+}
+
+ttt_status read_apply_chunk(ttt_pool *p, const ttt_group *g, int32_t layer, const void *X, const void *Vt,
+                            void *Y, void *stream) {
+  std::vector<OwnerRec *> recs;
+  ttt_status st = check_group(p, g, recs);
+  if (st != TTT_OK) return st;
+  const ttt_shape &sh = p->sh;
+  if (g->effect != TTT_WRITE) return fail(TTT_E_WRONG_EFFECT, "a whole chunk ends in its boundary WRITE");
+  if (layer < 0 || layer >= sh.n_layers) return fail(TTT_E_SHAPE, "layer out of range");
+  if (sh.dtype != TTT_BF16 || !read_chunk_supported(sh.d_model, sh.d_ff, sh.chunk))
+    return fail(TTT_E_SHAPE, "chunk READ needs bf16, d_ff % 64 == 0, d_model % 128 (or 160) == 0, C <= 128");
+  for (int b = 0; b < g->n; ++b) {
+    OwnerRec &r = *recs[b];
+    if (r.tail_len != 0 || (r.n_applied > 0 && !r.chunk_mode))
+      return fail(TTT_E_TAIL_FULL, "owner " + std::to_string(g->owner_map[b]) + " is not at a chunk start");
+    if (r.applied[layer]) return fail(TTT_E_ALREADY_APPLIED, "owner " + std::to_string(g->owner_map[b]));
+  }
+  if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  if (!X || !Vt || !Y) return fail(TTT_E_INVALID_ARG, "null X/Vt/Y");
+  ChunkLaunch cl{};
+  cl.n = g->n; cl.d_model = sh.d_model; cl.d_ff = sh.d_ff; cl.C = sh.chunk; cl.L = sh.n_layers; cl.layer = layer;
+  cl.max_slots = 2 * p->max_owners + p->n_ckpt;
+  cl.sel = p->d_sel();
+  cl.X = X; cl.Vt = Vt; cl.Y = Y;
+  cl.w_down = p->w_down;
+  cl.slots = p->arena + p->lay.slots;
+  cl.tailZ = p->arena + p->lay.tailZ;
+  cl.tailV = p->arena + p->lay.tailV;
+  cl.tz_owner = p->tz_owner; cl.tv_owner = p->tv_owner;
+  cl.tz_layer = (long long)layer * sh.chunk * sh.d_ff;
+  cl.tv_layer = (long long)layer * sh.chunk * sh.d_model;
+  for (int b = 0; b < g->n; ++b) cl.owner_idx[b] = recs[b]->idx;
+  cudaError_t e = launch_read_chunk(cl, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "read_chunk launch");
+  for (int b = 0; b < g->n; ++b) {
+    OwnerRec &r = *recs[b];
+    r.applied[layer] = 1;
+    r.n_applied += 1;
+    r.chunk_mode = true;
+    if (r.n_applied == sh.n_layers) r.tail_len = sh.chunk - 1;   // C entries in the tail; boundary token applied
   }
   return TTT_OK;
 }

@@ -92,6 +92,7 @@ def main():
     ap.add_argument("--read")
     ap.add_argument("--write")
     ap.add_argument("--launches")
+    ap.add_argument("--chunk")
     a = ap.parse_args()
     outdir = os.path.join(ROOT, "profiles", a.round)
     os.makedirs(outdir, exist_ok=True)
@@ -100,6 +101,8 @@ def main():
         traffic["read_decode_kernel"] = summarise(a.read, "read_decode", outdir)
     if a.write:
         traffic["write_tc_kernel"] = summarise(a.write, "write_tc", outdir)
+    if a.chunk:
+        traffic["read_chunk_tc_kernel"] = summarise(a.chunk, "read_chunk_tc", outdir)
     if a.launches:
         shutil.copy(a.launches, os.path.join(outdir, "launches.csv"))
         shares(a.launches, outdir)
