@@ -185,6 +185,11 @@ ttt_status read_apply(ttt_pool *pool, const ttt_group *g, int32_t layer, const v
 ttt_status read_apply_chunk(ttt_pool *pool, const ttt_group *g, int32_t layer, const void *X, const void *Vt,
                             void *Y, void *stream);
 
+/* NEXT f3 — streaming learner (C = 1): η used when read_apply of a WRITE group
+ * writes the candidate ΔW + η·v·xᵀ in the same pass (default 0.01f); the
+ * following write_commit must pass the same η and then only commits.        */
+ttt_status tttstate_set_eta(ttt_pool *pool, float eta);
+
 /* UpdateKVAndTailMetadata for a READ group once every layer was applied:
  * tail length += 1 per member (Alg. 1 line 13).                             */
 ttt_status tttstate_step_done(ttt_pool *pool, const ttt_group *g);

@@ -87,6 +87,7 @@ _sigs = {
                              C.POINTER(C.c_int32), P, C.POINTER(C.c_int32), P, P]),
     "tttstate_step_done": (C.c_int, [P, C.POINTER(ttt_group)]),
     "read_apply_chunk": (C.c_int, [P, C.POINTER(ttt_group), C.c_int32, P, P, P, P]),
+    "tttstate_set_eta": (C.c_int, [P, C.c_float]),
     "write_commit": (C.c_int, [P, C.POINTER(ttt_group), C.c_float, C.POINTER(C.c_uint32),
                                C.POINTER(C.c_uint64), P]),
     "tttstate_snapshot": (C.c_int, [P, C.c_uint64, P]),
@@ -274,6 +275,10 @@ def read_apply(pool, group: Group, layer: int, X, x_rows, Vt, v_rows, Y, y_rows=
 def read_apply_chunk(pool, group: Group, layer: int, X, Vt, Y, stream=None):
     """NEXT f2: all C tokens of each member's chunk at version v (tcgen05); then write_commit."""
     _check(_lib.read_apply_chunk(pool, C.byref(group.c), layer, _ptr(X), _ptr(Vt), _ptr(Y), _stream(stream)))
+
+
+def tttstate_set_eta(pool, eta: float):
+    _check(_lib.tttstate_set_eta(pool, C.c_float(eta)))
 
 
 def tttstate_step_done(pool, group: Group):

@@ -29,6 +29,9 @@ struct ReadParams {
   int owner_idx[kMaxReadMembers];
   int x_row[kMaxReadMembers], v_row[kMaxReadMembers], y_row[kMaxReadMembers];
   int tail_pos[kMaxReadMembers];
+  int fuse;                      // f3: also write ΔW + η·v·xᵀ to the shadow slot (C = 1)
+  float eta;
+  int *fail_flag;
 };
 
 // a5: chunk update of one layer for every member (shadow slot <- ΔW_v + η VᵀZ).

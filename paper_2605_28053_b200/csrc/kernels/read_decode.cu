@@ -95,7 +95,42 @@ template <> struct Elem<float> {
   __device__ static __forceinline__ float from_f(float v) { return v; }
 };
 
-template <typename T, int kThreads, int kU>
+// NEXT f3 — streaming learner (C = 1, every step a WRITE): with FUSE the delta
+// tasks also write the candidate row ΔW'[i] = ΔW[i] + η·v_i·x into the owner's
+// shadow slot while the pre-update row is in registers (y uses version v,
+// reading xvii), so an all-update step streams ΔW once in and once out instead
+// of READ + a separate WRITE pass (all-update row P:559).
+__device__ __forceinline__ uint32_t upd_bf16x2(uint32_t w, uint32_t x, float ev, uint32_t &expmax) {
+  const float lo = fmaf(ev, __uint_as_float(x << 16), __uint_as_float(w << 16));
+  const float hi = fmaf(ev, __uint_as_float(x & 0xffff0000u), __uint_as_float(w & 0xffff0000u));
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  expmax = __vmaxu2(expmax, r & 0x7f807f80u);
+  return r;
+}
+template <typename T> struct Upd;
+template <> struct Upd<__nv_bfloat16> {
+  __device__ static __forceinline__ uint4 apply(const uint4 &w, const uint4 &x, float ev, uint32_t &em) {
+    return make_uint4(upd_bf16x2(w.x, x.x, ev, em), upd_bf16x2(w.y, x.y, ev, em), upd_bf16x2(w.z, x.z, ev, em),
+                      upd_bf16x2(w.w, x.w, ev, em));
+  }
+  __device__ static __forceinline__ bool bad(uint32_t em) {
+    return (em & 0x7f80u) == 0x7f80u || (em >> 16) == 0x7f80u;
+  }
+};
+template <> struct Upd<float> {
+  __device__ static __forceinline__ uint32_t one(uint32_t w, uint32_t x, float ev, uint32_t &em) {
+    const float r = fmaf(ev, __uint_as_float(x), __uint_as_float(w));
+    em |= isfinite(r) ? 0u : 1u;
+    return __float_as_uint(r);
+  }
+  __device__ static __forceinline__ uint4 apply(const uint4 &w, const uint4 &x, float ev, uint32_t &em) {
+    return make_uint4(one(w.x, x.x, ev, em), one(w.y, x.y, ev, em), one(w.z, x.z, ev, em), one(w.w, x.w, ev, em));
+  }
+  __device__ static __forceinline__ bool bad(uint32_t em) { return em != 0; }
+};
+
+template <typename T, int kThreads, int kU, bool FUSE>
 __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadParams p) {
   constexpr int kWarps = kThreads / 32;
   using E = Elem<T>;
@@ -103,6 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint4 *xs = reinterpret_cast<uint4 *>(smem_raw);      // [n][nvec] member x rows
   __shared__ const uint4 *s_row0[kMaxReadMembers + 1];  // row-0 base of each matrix
+  __shared__ uint4 *s_dst0[kMaxReadMembers];             // FUSE: row-0 base of each shadow slot
 
   const int n = p.n, dff = p.d_ff, dm = p.d_model;
   const int nvec = dff / E::kVec;
@@ -116,6 +152,9 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
       const long long slot = 2LL * o + p.sel[o];
       s_row0[tid] = reinterpret_cast<const uint4 *>(static_cast<const T *>(p.slots) + slot * p.slot_elems +
                                                     p.layer_off);
+      if (FUSE)
+        s_dst0[tid - 1] = reinterpret_cast<uint4 *>(static_cast<T *>(const_cast<void *>(p.slots)) +
+                                                    (2LL * o + 1 - p.sel[o]) * p.slot_elems + p.layer_off);
     }
   }
   for (int idx = tid; idx < n * nvec; idx += kThreads) {
@@ -157,6 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
   Acc acc[kMaxReadMembers];
 #pragma unroll
   for (int r = 0; r < kMaxReadMembers; ++r) acc[r] = E::zero();
+  uint32_t expmax = 0;                             // FUSE: non-finite guard of the candidate
 
   while (true) {
     // next batch: same row, or the first batch of this warp's next task
@@ -186,6 +226,14 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
 #pragma unroll
       for (int u = 0; u < kU; ++u)                 // kU independent FMA chains
         if (v + 32 * u < nvec) E::dot(acc[u % kMaxReadMembers], cur[u], xb[v + 32 * u]);
+      if (FUSE) {
+        const int b = m - 1, i = t - m * dm;
+        const float ev = p.eta * E::to_f(static_cast<const T *>(p.Vt)[(size_t)p.v_row[b] * dm + i]);
+        uint4 *drow = s_dst0[b] + (size_t)i * nvec;
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (v + 32 * u < nvec) drow[v + 32 * u] = Upd<T>::apply(cur[u], xb[v + 32 * u], ev, expmax);
+      }
     }
 
     if (task_end) {
@@ -237,23 +285,30 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
     row = nrow;
     t = nt;
   }
+  if (FUSE && Upd<T>::bad(expmax)) atomicOr(p.fail_flag, 1);
 }
 
 size_t smem_bytes(int n, int d_ff, int esize) { return (size_t)n * d_ff * esize; }
 
-template <typename T, int TH, int U>
-cudaError_t launch_cfg(const ReadParams &p, cudaStream_t s) {
+template <typename T, int TH, int U, bool FUSE>
+cudaError_t launch_cfg1(const ReadParams &p, cudaStream_t s) {
   const size_t smem = smem_bytes(p.n, p.d_ff, sizeof(T));
   static int configured = -1;
   if ((int)smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(read_decode_kernel<T, TH, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(read_decode_kernel<T, TH, U, FUSE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return e;
     configured = (int)smem;
   }
-  read_decode_kernel<T, TH, U><<<device_sm_count(), TH, smem, s>>>(p);
+  read_decode_kernel<T, TH, U, FUSE><<<device_sm_count(), TH, smem, s>>>(p);
   count_launch();
   return cudaGetLastError();
+}
+
+template <typename T, int TH, int U>
+cudaError_t launch_cfg(const ReadParams &p, cudaStream_t s) {
+  return p.fuse ? launch_cfg1<T, TH, U, true>(p, s) : launch_cfg1<T, TH, U, false>(p, s);
 }
 
 int read_cfg() {

@@ -20,6 +20,7 @@ struct OwnerRec {
   std::vector<uint8_t> applied;   // per layer: current token appended
   int n_applied = 0;
   bool chunk_mode = false;    // current chunk applied by read_apply_chunk (f2)
+  int fused_layers = 0;       // f3: layers whose candidate read_apply already wrote (C = 1)
   bool has_ckpt = false;      // c_r^v
   uint64_t ckpt_v = 0;
   int ckpt_sel = 0;           // pinned pair slot (when ckpt_pool < 0)
@@ -47,6 +48,7 @@ struct ttt_pool {
   std::unordered_map<uint64_t, ttt::OwnerRec> owners;
   std::vector<int> free_idx, free_ckpt;
   int fail_seen = 0;
+  float eta = 0.01f;          // η used by the fused C = 1 path (tttstate_set_eta)
 
   // device pointers (valid when !host_only)
   unsigned char *slot_ptr(long long slot) const {

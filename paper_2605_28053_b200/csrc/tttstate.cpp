@@ -117,6 +117,20 @@ void clear_applied(OwnerRec &r) {
   std::fill(r.applied.begin(), r.applied.end(), 0);
   r.n_applied = 0;
   r.chunk_mode = false;
+  r.fused_layers = 0;
+}
+
+// A pinned checkpoint in the shadow slot must move to the checkpoint pool
+// before a WRITE overwrites the shadow (K5 checkpoint write).
+bool pinned_in_shadow(const OwnerRec &r) { return r.has_ckpt && r.ckpt_pool < 0 && r.ckpt_sel == 1 - r.sel; }
+
+cudaError_t evict_pinned(ttt_pool *p, OwnerRec &r, cudaStream_t s) {
+  const int c = p->free_ckpt.back();
+  p->free_ckpt.pop_back();
+  cudaError_t e = launch_copy(p->slot_ptr(2LL * p->max_owners + c), p->slot_ptr(2LL * r.idx + r.ckpt_sel),
+                              p->slot_bytes(), s);
+  r.ckpt_pool = c;
+  return e;
 }
 
 }  // namespace
@@ -335,9 +349,19 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
     if (r.applied[layer]) return fail(TTT_E_ALREADY_APPLIED, "owner " + std::to_string(g->owner_map[b]));
     if (r.chunk_mode) return fail(TTT_E_WRONG_EFFECT, "owner " + std::to_string(g->owner_map[b]) + " is mid-chunk");
   }
+  // f3: with C = 1 every step is a WRITE whose evidence is this token only, so the
+  // candidate is written here, in the same pass over ΔW (write_commit then only commits).
+  const bool fuse = g->effect == TTT_WRITE && sh.chunk == 1 && g_write_impl.load() != 1;
+  int need_evict = 0;
+  if (fuse)
+    for (int b = 0; b < g->n; ++b) need_evict += (recs[b]->n_applied == 0 && pinned_in_shadow(*recs[b]));
+  if (need_evict > (int)p->free_ckpt.size()) return fail(TTT_E_POOL_FULL, "no free checkpoint slot for a pinned snapshot");
   if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
   if (!X || !Vt || !Y) return fail(TTT_E_INVALID_ARG, "null X/Vt/Y");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (fuse)
+    for (int b = 0; b < g->n; ++b)
+      if (recs[b]->n_applied == 0 && pinned_in_shadow(*recs[b])) CUDA_TRY(evict_pinned(p, *recs[b], s));
   int per = std::min(kMaxReadMembers, g->n);
   while (per > 1 && !read_decode_fits(per, sh.d_model, sh.d_ff, (int)p->esize)) --per;
   if (!read_decode_fits(per, sh.d_model, sh.d_ff, (int)p->esize))
@@ -360,6 +384,9 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
     rp.tickets = reinterpret_cast<int *>(p->arena + p->lay.tickets);
     rp.n = std::min(per, g->n - b0);
     rp.d_model = sh.d_model; rp.d_ff = sh.d_ff;
+    rp.fuse = fuse ? 1 : 0;
+    rp.eta = p->eta;
+    rp.fail_flag = p->d_fail_flag();
     for (int k = 0; k < rp.n; ++k) {
       const int b = b0 + k;
       rp.owner_idx[k] = recs[b]->idx;
@@ -374,7 +401,14 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
   for (int b = 0; b < g->n; ++b) {
     recs[b]->applied[layer] = 1;
     recs[b]->n_applied += 1;
+    if (fuse) recs[b]->fused_layers += 1;
   }
+  return TTT_OK;
+}
+
+ttt_status tttstate_set_eta(ttt_pool *p, float eta) {
+  if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
+  p->eta = eta;
   return TTT_OK;
 }
 
@@ -444,52 +478,49 @@ ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32
   if (st != TTT_OK) return st;
   const ttt_shape &sh = p->sh;
   if (g->effect != TTT_WRITE) return fail(TTT_E_WRONG_EFFECT, "write_commit needs a WRITE group");
-  int need_evict = 0;
+  int need_evict = 0, n_fused = 0;
   for (int b = 0; b < g->n; ++b) {
     OwnerRec &r = *recs[b];
     if (r.tail_len != sh.chunk - 1) return fail(TTT_E_TAIL_NOT_FULL, "owner " + std::to_string(g->owner_map[b]));
     if (r.n_applied != sh.n_layers) return fail(TTT_E_NOT_APPLIED, "owner " + std::to_string(g->owner_map[b]));
-    if (r.has_ckpt && r.ckpt_pool < 0 && r.ckpt_sel == 1 - r.sel) ++need_evict;
+    need_evict += pinned_in_shadow(r);
+    n_fused += r.fused_layers == sh.n_layers;
   }
-  if (need_evict > (int)p->free_ckpt.size()) return fail(TTT_E_POOL_FULL, "no free checkpoint slot for a pinned snapshot");
+  const bool fused = n_fused == g->n;               // every candidate already written by read_apply (f3)
+  if (n_fused != 0 && !fused) return fail(TTT_E_INVALID_ARG, "group mixes fused and unfused members");
+  if (fused && eta != p->eta) return fail(TTT_E_INVALID_ARG, "eta differs from the pool's fused-path eta");
+  if (!fused && need_evict > (int)p->free_ckpt.size())
+    return fail(TTT_E_POOL_FULL, "no free checkpoint slot for a pinned snapshot");
+  const int impl = g_write_impl.load();
+  const bool use_tc = sh.dtype == TTT_BF16 && impl != 1 && write_tc_supported(sh.d_model, sh.d_ff, sh.chunk);
+  if (!fused && impl == 2 && !use_tc) return fail(TTT_E_SHAPE, "tcgen05 WRITE kernel does not support this shape");
   bool forced = false;
   if (fail_mask)
     for (int b = 0; b < g->n; ++b) forced |= (fail_mask[b / 32] >> (b % 32)) & 1u;
   if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-
-  // preserve pinned checkpoints that sit in the shadow slot (K5 checkpoint write)
-  for (int b = 0; b < g->n; ++b) {
-    OwnerRec &r = *recs[b];
-    if (r.has_ckpt && r.ckpt_pool < 0 && r.ckpt_sel == 1 - r.sel) {
-      const int c = p->free_ckpt.back();
-      p->free_ckpt.pop_back();
-      CUDA_TRY(launch_copy(p->slot_ptr(2LL * p->max_owners + c), p->slot_ptr(2LL * r.idx + r.ckpt_sel),
-                           p->slot_bytes(), s));
-      r.ckpt_pool = c;
+  if (!fused) {
+    for (int b = 0; b < g->n; ++b)                  // preserve pinned checkpoints sitting in the shadow slot
+      if (pinned_in_shadow(*recs[b])) CUDA_TRY(evict_pinned(p, *recs[b], s));
+    WriteParams wp{};
+    wp.slots = p->arena + p->lay.slots;
+    wp.slot_elems = p->slot_elems;
+    wp.sel = p->d_sel();
+    wp.tailZ = p->arena + p->lay.tailZ;
+    wp.tailV = p->arena + p->lay.tailV;
+    wp.tz_owner = p->tz_owner; wp.tv_owner = p->tv_owner;
+    wp.eta = eta;
+    wp.fail_flag = p->d_fail_flag();
+    wp.n = g->n; wp.d_model = sh.d_model; wp.d_ff = sh.d_ff; wp.C = sh.chunk;
+    wp.max_owners = p->max_owners; wp.max_slots = 2 * p->max_owners + p->n_ckpt;
+    for (int b = 0; b < g->n; ++b) wp.owner_idx[b] = recs[b]->idx;
+    for (int l = 0; l < sh.n_layers; ++l) {
+      wp.layer_off = (long long)l * p->E;
+      wp.tz_layer = (long long)l * sh.chunk * sh.d_ff;
+      wp.tv_layer = (long long)l * sh.chunk * sh.d_model;
+      cudaError_t e = use_tc ? launch_write_tc(wp, s) : launch_write_simt(sh.dtype, wp, s);
+      if (e != cudaSuccess) return cuda_fail(e, "write launch");
     }
-  }
-  WriteParams wp{};
-  wp.slots = p->arena + p->lay.slots;
-  wp.slot_elems = p->slot_elems;
-  wp.sel = p->d_sel();
-  wp.tailZ = p->arena + p->lay.tailZ;
-  wp.tailV = p->arena + p->lay.tailV;
-  wp.tz_owner = p->tz_owner; wp.tv_owner = p->tv_owner;
-  wp.eta = eta;
-  wp.fail_flag = p->d_fail_flag();
-  wp.n = g->n; wp.d_model = sh.d_model; wp.d_ff = sh.d_ff; wp.C = sh.chunk;
-  wp.max_owners = p->max_owners; wp.max_slots = 2 * p->max_owners + p->n_ckpt;
-  for (int b = 0; b < g->n; ++b) wp.owner_idx[b] = recs[b]->idx;
-  const int impl = g_write_impl.load();
-  const bool use_tc = sh.dtype == TTT_BF16 && impl != 1 && write_tc_supported(sh.d_model, sh.d_ff, sh.chunk);
-  if (impl == 2 && !use_tc) return fail(TTT_E_SHAPE, "tcgen05 WRITE kernel does not support this shape");
-  for (int l = 0; l < sh.n_layers; ++l) {
-    wp.layer_off = (long long)l * p->E;
-    wp.tz_layer = (long long)l * sh.chunk * sh.d_ff;
-    wp.tv_layer = (long long)l * sh.chunk * sh.d_model;
-    cudaError_t e = use_tc ? launch_write_tc(wp, s) : launch_write_simt(sh.dtype, wp, s);
-    if (e != cudaSuccess) return cuda_fail(e, "write launch");
   }
   CommitParams cp{};
   cp.sel = p->d_sel();

@@ -38,6 +38,7 @@ class Engine:
         self.w_down = w_down
         self.pool = capi.tttstate_pool_create(self.shape, shape_id, placement, max_owners, n_ckpt, base,
                                               self.arena_bytes, w_down)
+        capi.tttstate_set_eta(self.pool, self.eta)
         self.planner = capi.ttt_planner_create(mode, B, w)
         capi.ttt_planner_attach(self.planner, self.pool)
         self.shape_id, self.placement, self.device = shape_id, placement, device

@@ -177,3 +177,19 @@ def test_generator_device_matches_numpy():
             ref = rng.gen(11, t, o, l, p, (n,), amp, "bf16" if bf16 else "fp32")
             got = out.view(torch.int16).cpu().numpy().view(np.uint16) if bf16 else out.cpu().numpy()
             assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("impl", [0, 1])   # 0: fused C=1 READ+WRITE (f3), 1: separate SIMT WRITE
+def test_all_update_streaming_learner_controls(dtype, impl):
+    tr = T.uniform_small(n_streams=5, n_layers=2, d_model=128, d_ff=192, chunk=1, n_steps=9, dtype=dtype,
+                         delta0="rng", seed=12, v0=3,
+                         controls={(0, 2): ["snapshot"], (0, 5): ["rollback"], (1, 1): ["fail"], (3, 0): ["snapshot"],
+                                   (3, 4): ["rollback"], (4, 6): ["fail"], (2, 3): ["snapshot"]})
+    prev = capi.tttstate_set_write_impl(impl)
+    try:
+        ref, src, log, eng = _run(tr)
+    finally:
+        capi.tttstate_set_write_impl(prev)
+    _compare(tr, ref, src, log, eng)
+    assert log.fallbacks == 2
