@@ -111,19 +111,61 @@ def config2_paper(seed: int = 0, n_steps: int = 512, n_layers: int = 36) -> Trac
                  n_steps=n_steps, dtype="bf16", seed=seed, v0=256, delta0="rng", B=8, w=0)
 
 
-def config3_interleaved(seed: int = 0, n_steps: int = 512, n_layers: int = 12, w: int = 4) -> Trace:
-    """BJ configs[2]: 64 streams, L=12 (memory), bursty offsets, failures, rollbacks."""
-    offs = bursty_offsets(64, 128, seed)
+def config3_interleaved(seed: int = 0, n_steps: int = 512, n_layers: int = 12, w: int = 4,
+                        d_model: int = 2560, d_ff: int = 9728, chunk: int = 128) -> Trace:
+    """BJ configs[2]: 64 streams, L=12 (memory), bursty offsets, injected write
+    failures on 1/16 of the streams' first boundary, speculative snapshot + rollback on 1/8."""
+    offs = bursty_offsets(64, chunk, seed)
     ctl = {}
     for s in range(0, 64, 16):                     # injected write failures
-        ctl.setdefault((s, 128 - 1 - offs[s]), []).append("fail")
+        ctl.setdefault((s, chunk - 1 - offs[s]), []).append("fail")
     for s in range(3, 64, 8):                      # speculative snapshot + rollback
-        p = 128 - 1 - offs[s]
+        p = chunk - 1 - offs[s]
         ctl.setdefault((s, p), []).append("snapshot")
         ctl.setdefault((s, p + 1), []).append("rollback")
-    return Trace("config3_interleaved", n_streams=64, n_layers=n_layers, d_model=2560, d_ff=9728,
-                 chunk=128, n_steps=n_steps, dtype="bf16", seed=seed, v0=0, delta0="rng",
+    return Trace("config3_interleaved", n_streams=64, n_layers=n_layers, d_model=d_model, d_ff=d_ff,
+                 chunk=chunk, n_steps=n_steps, dtype="bf16", seed=seed, v0=0, delta0="rng",
                  offsets=offs, controls=ctl, B=64, w=w)
+
+
+def config5_sharded(seed: int = 0, n_steps: int = 512, n_layers: int = 4, d_model: int = 2560,
+                    d_ff: int = 9728, chunk: int = 128, n_streams: int = 256) -> Trace:
+    """BJ configs[4]: 256 streams sharded by owner over G GPUs, 64K context (v0 = 512), uniform."""
+    return Trace("config5_sharded", n_streams=n_streams, n_layers=n_layers, d_model=d_model, d_ff=d_ff,
+                 chunk=chunk, n_steps=n_steps, dtype="bf16", seed=seed, v0=512, delta0="rng", B=n_streams, w=0)
+
+
+def shard(tr: Trace, world: int, rank: int) -> Trace:
+    """The streams placed on `rank` (π(o) = s mod world) as a trace of their own; owner ids and
+    inputs are unchanged because streams keep their global index via owner_base + s."""
+    mine = [s for s in range(tr.n_streams) if s % world == rank]
+    return ShardTrace(tr, mine)
+
+
+class ShardTrace(Trace):
+    """A Trace restricted to a subset of the streams (local index k -> global stream mine[k])."""
+
+    def __init__(self, base: Trace, mine):
+        import dataclasses as _dc
+        fields = {f.name: getattr(base, f.name) for f in _dc.fields(base)}
+        fields["n_streams"] = len(mine)
+        fields["B"] = min(base.B, len(mine))
+        fields["offsets"] = tuple(base.offset(s) for s in mine) if base.offsets else ()
+        fields["controls"] = {(mine.index(s), p): ops for (s, p), ops in base.controls.items() if s in mine}
+        super().__init__(**fields)
+        self.base, self.mine = base, list(mine)
+
+    def owner(self, s):
+        return self.base.owner(self.mine[s])
+
+    def delta0_of(self, s, l):
+        return self.base.delta0_of(self.mine[s], l)
+
+    def x(self, s, p, l):
+        return self.base.x(self.mine[s], p, l)
+
+    def tgt(self, s, p, l):
+        return self.base.tgt(self.mine[s], p, l)
 
 
 def uniform_small(seed=0, n_streams=8, n_layers=2, d_model=128, d_ff=320, chunk=8, n_steps=24,
