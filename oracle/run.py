@@ -34,6 +34,7 @@ class Record:
     versions: dict = field(default_factory=dict)     # s -> final V
     state: dict = field(default_factory=dict)        # s -> [per layer ΔW float64]
     events: dict = field(default_factory=dict)       # (s, p) -> effect
+    branches: dict = field(default_factory=dict)     # live branch owner -> (v, [payload per layer])
 
 
 def make_table(tr: Trace, layers=None) -> StateTable:
@@ -42,13 +43,19 @@ def make_table(tr: Trace, layers=None) -> StateTable:
         W = [np.eye(tr.d_model, tr.d_ff) for _ in layers]
     else:
         W = [nm.widen(tr.w_down(l), tr.dtype) for l in layers]
-    return StateTable(len(W), tr.d_model, tr.d_ff, tr.chunk, tr.dtype, W, tr.eta, tr.rule)
+    return StateTable(len(W), tr.d_model, tr.d_ff, tr.chunk, tr.dtype, W, tr.eta, tr.rule,
+                      backend=tr.backend, rank=tr.rank)
 
 
 def init_stream(tab: StateTable, tr: Trace, s: int, layers=None):
     layers = list(range(tr.n_layers)) if layers is None else list(layers)
     d0 = [tr.delta0_of(s, l) for l in layers]
-    init = None if d0[0] is None else [nm.widen(d, tr.dtype) for d in d0]
+    if d0[0] is None:
+        init = None
+    elif tr.backend == 1:
+        init = [(nm.widen(a, tr.dtype), nm.widen(b, tr.dtype)) for a, b in d0]
+    else:
+        init = [nm.widen(d, tr.dtype) for d in d0]
     tab.alloc(tr.owner(s), init, tr.v0)
     off = tr.offset(s)
     if off:
@@ -64,8 +71,9 @@ def _inputs(tr: Trace, s: int, p: int, layers):
     return zs, vs
 
 
-def _control(tab, tr, rec, s, p):
+def _control(tab, tr, rec, s, p, forks=None):
     r = tr.owner(s)
+    forks = {} if forks is None else forks
     for op in tr.controls_at(s, p):
         if op == "snapshot":
             tab.snapshot(r)
@@ -73,6 +81,18 @@ def _control(tab, tr, rec, s, p):
             v_before = tab.version(r)
             v_after = tab.rollback(r)
             rec.commits.append((s, p, v_before, v_after, "rolled_back"))
+        elif op == "fork":                                  # new owner/version lineage
+            k = forks.get(s, 0)
+            tab.fork(r, tr.branch_owner(s, k))
+            forks[s] = k + 1
+        elif op == "release":                               # free the stream's latest branch
+            tab.free(tr.branch_owner(s, forks[s] - 1))
+
+
+def _branches(tab, tr, rec):
+    for b, o in tab.owners.items():
+        if b >= tr.owner_base + 1_000_000:
+            rec.branches[b] = (o.v, [tuple(x.copy() for x in S) if isinstance(S, tuple) else S.copy() for S in o.S])
 
 
 def run_sequential(tr: Trace, layers=None, keep_outputs: bool = True, streams=None) -> Record:
@@ -80,11 +100,12 @@ def run_sequential(tr: Trace, layers=None, keep_outputs: bool = True, streams=No
     layers = list(range(tr.n_layers)) if layers is None else list(layers)
     tab = make_table(tr, layers)
     rec = Record()
+    forks: dict = {}
     for s in (range(tr.n_streams) if streams is None else streams):
         init_stream(tab, tr, s, layers)
         r = tr.owner(s)
         for p in range(tr.n_steps):
-            _control(tab, tr, rec, s, p)
+            _control(tab, tr, rec, s, p, forks)
             eff = tab.next_effect(r)
             rec.events[(s, p)] = eff
             zs, vs = _inputs(tr, s, p, layers)
@@ -103,8 +124,13 @@ def run_sequential(tr: Trace, layers=None, keep_outputs: bool = True, streams=No
                 tab.write_group([r])
                 rec.commits.append((s, p, v, v + 1, "ok"))
         rec.versions[s] = tab.version(r)
-        rec.state[s] = [x.copy() for x in tab.owners[r].S]
+        rec.state[s] = _state_copy(tab.owners[r].S)
+    _branches(tab, tr, rec)
     return rec
+
+
+def _state_copy(S):
+    return [tuple(a.copy() for a in x) if isinstance(x, tuple) else x.copy() for x in S]
 
 
 def run_batched(tr: Trace, layers=None, keep_outputs: bool = True) -> Record:
@@ -118,6 +144,7 @@ def run_batched(tr: Trace, layers=None, keep_outputs: bool = True) -> Record:
     pos = [0] * tr.n_streams
     pending = set()
     failed_once = set()
+    forks: dict = {}
 
     def V(r):
         return tab.version(r) if r in tab.owners else None
@@ -127,9 +154,9 @@ def run_batched(tr: Trace, layers=None, keep_outputs: bool = True) -> Record:
         events = []
         for s in range(tr.n_streams):                       # View + NextStep
             if pos[s] < tr.n_steps and s not in pending:
-                _control(tab, tr, rec, s, pos[s])
+                _control(tab, tr, rec, s, pos[s], forks)
                 r = tr.owner(s)
-                events.append(Event(r, tab.next_effect(r), 0, 0, 0, tab.version(r), clock))
+                events.append(Event(r, tab.next_effect(r), tr.backend, 0, 0, tab.version(r), clock))
                 pending.add(s)
         groups, rejected = planner.plan(events, clock, V)   # LegalGroups
         assert not rejected, rejected
@@ -167,7 +194,8 @@ def run_batched(tr: Trace, layers=None, keep_outputs: bool = True) -> Record:
         clock += 1
     for s in range(tr.n_streams):
         rec.versions[s] = tab.version(tr.owner(s))
-        rec.state[s] = [x.copy() for x in tab.owners[tr.owner(s)].S]
+        rec.state[s] = _state_copy(tab.owners[tr.owner(s)].S)
+    _branches(tab, tr, rec)
     return rec
 
 

@@ -21,9 +21,19 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import lowrank as lr
 from . import numerics as nm
 
 READ, WRITE = 0, 1
+
+
+def _copy(S):
+    """Deep copy of one owner's payload (per layer: ΔW array, or (A, B) for low rank)."""
+    return [tuple(np.array(a, copy=True) for a in x) if isinstance(x, tuple) else x.copy() for x in S]
+
+
+def _finite(x) -> bool:
+    return all(np.all(np.isfinite(a)) for a in x) if isinstance(x, tuple) else bool(np.all(np.isfinite(x)))
 
 
 class ContractError(Exception):
@@ -46,9 +56,10 @@ class Owner:
 
 class StateTable:
     def __init__(self, n_layers: int, d_model: int, d_ff: int, chunk: int, dtype: str,
-                 w_down: list, eta: float, rule: int = 0):
+                 w_down: list, eta: float, rule: int = 0, backend: int = 0, rank: int = 0):
         self.L, self.dm, self.dff, self.C = n_layers, d_model, d_ff, chunk
         self.dtype, self.eta, self.rule = dtype, float(eta), rule
+        self.backend, self.rank = backend, rank          # τ: 0 fast weights, 1 low-rank delta (NEXT f1)
         self.W = w_down                      # per layer float64 (identity for rule 1)
         self.owners: dict[int, Owner] = {}
 
@@ -57,8 +68,13 @@ class StateTable:
         """register -> v=0, or given init bytes with v0 (reading v)."""
         if r in self.owners:
             raise ContractError("DUPLICATE_OWNER", str(r))
-        S = [np.zeros((self.dm, self.dff)) if init is None else np.array(init[l], dtype=np.float64)
-             for l in range(self.L)]
+        if self.backend == 1:
+            S = [(np.zeros((self.rank, self.dff)), np.zeros((self.rank, self.dm))) if init is None else
+                 (np.array(init[l][0], dtype=np.float64), np.array(init[l][1], dtype=np.float64))
+                 for l in range(self.L)]
+        else:
+            S = [np.zeros((self.dm, self.dff)) if init is None else np.array(init[l], dtype=np.float64)
+                 for l in range(self.L)]
         self.owners[r] = Owner(v=v0, S=S)
         return v0
 
@@ -88,7 +104,10 @@ class StateTable:
         o = self._get(r)
         if len(o.tail_p) >= self.C:
             raise ContractError("TAIL_FULL", str(r))
-        ys = [nm.apply_read(self.W[l], o.S[l], zs[l], self.rule) for l in range(self.L)]
+        if self.backend == 1:
+            ys = [lr.apply_read(self.W[l], o.S[l][0], o.S[l][1], zs[l]) for l in range(self.L)]
+        else:
+            ys = [nm.apply_read(self.W[l], o.S[l], zs[l], self.rule) for l in range(self.L)]
         o.tail_z.append(list(zs))
         o.tail_v.append(list(vs))
         o.tail_p.append(p)
@@ -113,8 +132,11 @@ class StateTable:
             for l in range(self.L):
                 Z = np.stack([e[l] for e in o.tail_z])     # [C, d_ff]
                 V = np.stack([e[l] for e in o.tail_v])     # [C, d_model]
-                cands[r].append(nm.boundary_update(o.S[l], Z, V, self.eta, self.dtype, self.rule))
-        if fail or any(not all(np.all(np.isfinite(c)) for c in cands[r]) for r in members):
+                if self.backend == 1:
+                    cands[r].append(lr.boundary_update(o.S[l][0], o.S[l][1], Z, self.eta, self.dtype))
+                else:
+                    cands[r].append(nm.boundary_update(o.S[l], Z, V, self.eta, self.dtype, self.rule))
+        if fail or any(not all(_finite(c) for c in cands[r]) for r in members):
             raise ContractError("WRITE_FAILED", str(members))
         out = []
         for r in members:
@@ -129,7 +151,7 @@ class StateTable:
     def snapshot(self, r: int):
         """c_r^v <- s_r^v; latest wins."""
         o = self._get(r)
-        o.ckpt = (o.v, [s.copy() for s in o.S])
+        o.ckpt = (o.v, _copy(o.S))
 
     def rollback(self, r: int) -> int:
         """Restore the checkpointed slot and version; clear tail (reading vii)."""
@@ -137,7 +159,7 @@ class StateTable:
         if o.ckpt is None:
             raise ContractError("NO_CHECKPOINT", str(r))
         o.v = o.ckpt[0]
-        o.S = [s.copy() for s in o.ckpt[1]]
+        o.S = _copy(o.ckpt[1])
         o.tail_z, o.tail_v, o.tail_p = [], [], []
         return o.v
 
@@ -146,7 +168,7 @@ class StateTable:
         o = self._get(src)
         if dst in self.owners:
             raise ContractError("DUPLICATE_OWNER", str(dst))
-        self.owners[dst] = Owner(v=o.v, S=[s.copy() for s in o.S])
+        self.owners[dst] = Owner(v=o.v, S=_copy(o.S))
         return o.v
 
     def prefill_tail(self, r: int, zs_list: list, vs_list: list, ps: list):

@@ -354,3 +354,62 @@ def test_planner_property_eq3_eq4_random():
 def test_normwise_metric():
     assert nm.normwise_rel_err(np.array([1.0, 2.0]), np.array([1.0, 2.0])) == 0.0
     assert nm.normwise_rel_err(np.array([1.0, 2.1]), np.array([1.0, 2.0])) == pytest.approx(0.05)
+
+
+# ---------------------------------------------------------------- low-rank delta (NEXT f1)
+from oracle import lowrank as lr  # noqa: E402
+
+
+def test_lowrank_spec_examples_square_identity_base():
+    # y = x + Bᵀ(A x) with the identity base; A = 0 -> y = x for any B
+    rs = np.random.default_rng(30)
+    d, R = 4, 2
+    x = rs.integers(-4, 4, d) / 4.0
+    B = rs.integers(-4, 4, (R, d)) / 4.0
+    assert np.array_equal(lr.apply_read(np.eye(d), np.zeros((R, d)), B, x), x)
+    A = rs.integers(-4, 4, (R, d)) / 4.0
+    assert np.array_equal(lr.apply_read(np.eye(d), A, B, x), x + B.T @ (A @ x))
+
+
+def test_lowrank_exact_rational_brute_force_nonsquare():
+    rs = np.random.default_rng(31)
+    dm, dff, R, C = 3, 5, 2, 4
+    W = rs.integers(-4, 4, (dm, dff)) / 8.0
+    A = rs.integers(-4, 4, (R, dff)) / 8.0
+    B = rs.integers(-4, 4, (R, dm)) / 8.0
+    z = rs.integers(-4, 4, dff) / 4.0
+    y = lr.apply_read(W, A, B, z)
+    for i in range(dm):
+        ref = sum(Fraction(W[i, j]) * Fraction(z[j]) for j in range(dff))
+        ref += sum(Fraction(B[k, i]) * sum(Fraction(A[k, j]) * Fraction(z[j]) for j in range(dff)) for k in range(R))
+        assert Fraction(y[i]) == ref
+    Z = rs.integers(-4, 4, (C, dff)) / 4.0
+    eta = 2.0 ** -3
+    A2, B2 = lr.boundary_update(A, B, Z, eta, "fp32")
+    m = [sum(Fraction(Z[t, j]) for t in range(C)) / C for j in range(dff)]
+    for k in range(R):
+        am = sum(Fraction(A[k, j]) * m[j] for j in range(dff))
+        for j in range(dff):
+            assert Fraction(A2[k, j]) == Fraction(A[k, j]) + Fraction(eta) * am * m[j]
+    assert np.array_equal(B2, B)                                # B' = B
+
+
+def test_lowrank_spec_update_example_s219_generalised():
+    # A = I (2x2), m = (1,1), η = 0.01: A' = I + η·(A m) mᵀ = I + 0.01·ones (fp32 storage)
+    eta = float(np.float32(0.01))
+    A2, _ = lr.boundary_update(np.eye(2), np.zeros((2, 2)), np.array([[1.0, 1.0], [1.0, 1.0]]), eta, "fp32")
+    assert np.array_equal(A2, (np.eye(2) + eta * np.ones((2, 2))).astype(np.float32).astype(np.float64))
+
+
+def test_config4_branches_sequential_equals_batched():
+    tr = T.config4_lowrank(n_steps=20, n_layers=2, rank=4, d_model=12, d_ff=16, chunk=4, n_streams=6, seed=3)
+    a, b = run_sequential(tr), run_batched(tr)
+    assert a.versions == b.versions and ok_commits(a) == ok_commits(b)
+    for k in a.outputs:
+        assert np.array_equal(a.outputs[k], b.outputs[k])
+    assert set(a.branches) == set(b.branches) and len(a.branches) == tr.n_streams   # one live branch each
+    for br, (v, S) in a.branches.items():
+        assert b.branches[br][0] == v
+        for l in range(tr.n_layers):
+            assert all(np.array_equal(x, y) for x, y in zip(S[l], b.branches[br][1][l]))
+    assert any(c[4] == "rolled_back" for c in a.commits)

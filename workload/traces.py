@@ -44,6 +44,8 @@ class Trace:
     mode: int = MODE_FULL
     rule: int = 0                # 0: chunk sum of outer products (reading i); 1: SPEC mean rule
     owner_base: int = 1000       # owner id of stream s is owner_base + s
+    backend: int = 0             # τ: 0 fast weights (ΔW), 1 low-rank delta (A, B) — NEXT f1
+    rank: int = 0                # R for the low-rank backend
 
     def replace(self, **kw) -> "Trace":
         return dataclasses.replace(self, **kw)
@@ -64,9 +66,18 @@ class Trace:
         return rng.gen(self.seed, rng.T_W_DOWN, 0, l, 0, (self.d_model, self.d_ff), self.amp_w, self.dtype)
 
     def delta0_of(self, s: int, l: int):
+        """Initial payload of layer l: ΔW_0, or (A_0, B_0) for the low-rank backend."""
         if self.delta0 == "zero":
             return None
+        if self.backend == 1:
+            return (rng.gen(self.seed, rng.T_LR_A, self.owner(s), l, 0, (self.rank, self.d_ff), self.amp_w, self.dtype),
+                    rng.gen(self.seed, rng.T_LR_B, self.owner(s), l, 0, (self.rank, self.d_model),
+                            rng.amp_inv_sqrt(self.rank), self.dtype))
         return rng.gen(self.seed, rng.T_DELTA0, self.owner(s), l, 0, (self.d_model, self.d_ff), self.amp_w, self.dtype)
+
+    def branch_owner(self, s: int, k: int) -> int:
+        """Owner id of stream s's k-th forked branch lineage."""
+        return self.owner(s) + 1_000_000 * (k + 1)
 
     def x(self, s: int, p: int, l: int) -> np.ndarray:
         """READ input z for stream s at position p, layer l (p < 0: pre-filled tail)."""
@@ -133,6 +144,30 @@ def config5_sharded(seed: int = 0, n_steps: int = 512, n_layers: int = 4, d_mode
     """BJ configs[4]: 256 streams sharded by owner over G GPUs, 64K context (v0 = 512), uniform."""
     return Trace("config5_sharded", n_streams=n_streams, n_layers=n_layers, d_model=d_model, d_ff=d_ff,
                  chunk=chunk, n_steps=n_steps, dtype="bf16", seed=seed, v0=512, delta0="rng", B=n_streams, w=0)
+
+
+def config4_lowrank(seed: int = 0, n_steps: int = 512, n_layers: int = 36, rank: int = 16,
+                    d_model: int = 2560, d_ff: int = 9728, chunk: int = 128, n_streams: int = 128,
+                    accept_p: float = 0.75) -> Trace:
+    """BJ configs[3]: low-rank delta TTTState (R = 16 or 64), 128 streams, speculative branch
+    versions: at every boundary each stream forks a branch lineage and snapshots; the
+    speculative WRITE is accepted with p = 0.75 (seeded) or rolled back; the previous
+    boundary's branch is released (reading xix)."""
+    ctl = {}
+    u = rng.raw_u24(seed, 98, 0, 0, 0, n_streams * (n_steps // chunk + 1)) + (1 << 23)
+    k = 0
+    for s in range(n_streams):
+        for b, p in enumerate(range(chunk - 1, n_steps, chunk)):
+            ops = ctl.setdefault((s, p), [])
+            if b > 0:
+                ops.append("release")
+            ops += ["fork", "snapshot"]
+            if u[k] / float(1 << 24) >= accept_p and p + 1 < n_steps:
+                ctl.setdefault((s, p + 1), []).append("rollback")
+            k += 1
+    return Trace("config4_lowrank", n_streams=n_streams, n_layers=n_layers, d_model=d_model, d_ff=d_ff,
+                 chunk=chunk, n_steps=n_steps, dtype="bf16", seed=seed, v0=0, delta0="rng", controls=ctl,
+                 B=n_streams, w=0, backend=1, rank=rank)
 
 
 def shard(tr: Trace, world: int, rank: int) -> Trace:
