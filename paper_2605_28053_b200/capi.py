@@ -332,6 +332,13 @@ def tttstate_read_payload(pool, owner: int, layer: int, d_model: int, d_ff: int,
     return out
 
 
+def tttstate_read_payload_flat(pool, owner: int, layer: int, n_elems: int, dtype, stream=None):
+    """Committed payload of one layer as a flat array (low-rank: A [R·d_ff] then B [R·d_model])."""
+    out = np.empty((n_elems,), dtype=_np_dtype(dtype))
+    _check(_lib.tttstate_read_payload(pool, owner, layer, out.ctypes.data, _stream(stream)))
+    return out
+
+
 def tttstate_read_slot_raw(pool, owner: int, which: int, layer: int, d_model: int, d_ff: int, dtype, stream=None):
     out = np.empty((d_model, d_ff), dtype=_np_dtype(dtype))
     _check(_lib.tttstate_read_slot_raw(pool, owner, which, layer, out.ctypes.data, _stream(stream)))

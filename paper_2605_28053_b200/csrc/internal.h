@@ -10,6 +10,7 @@ namespace ttt {
 
 constexpr int kMaxReadMembers = 8;     // members per READ launch (X rows staged in smem)
 constexpr int kMaxGroup = 256;         // members per group (planner B cap)
+constexpr int kMaxKSplit = 16;         // low-rank base GEMM split-K slabs
 
 // a3 + a4: decode READ over one layer for ≤ kMaxReadMembers members.
 struct ReadParams {
@@ -66,8 +67,43 @@ struct ChunkLaunch {
   const void *X, *Vt, *w_down, *slots;
   void *Y, *tailZ, *tailV;
   long long tz_owner, tv_owner, tz_layer, tv_layer;
+  int delta = 1;                 // 0: base product only (low-rank READ's X·W_downᵀ)
+  int append = 1;                // append the chunk to the tail
+  float *Y32 = nullptr;          // non-null: fp32 output rows b*C + t (< valid_rows) instead of bf16 Y
+  int valid_rows = 0;
+  int ksplit = 1;                // base mode: K split in `ksplit` ranges, slab ks at Y32 + ks*y32_slab
+  long long y32_slab = 0;
   int owner_idx[kMaxGroup];
 };
+
+// NEXT f1: low-rank delta READ / WRITE (DeltaAdapterState).
+struct LowRankRead {
+  int n, d_model, d_ff, rank;
+  const void *X, *Vt, *resid;
+  void *Y, *Xg;
+  float *Y32, *u;                // [ksplit][rows][d_model] base product slabs, [n][64] A·x
+  int ksplit;
+  long long y32_slab;
+  const void *slots;
+  long long slot_elems, layer_off;
+  const int *sel;
+  void *tailZ, *tailV;
+  long long tz_owner, tv_owner, tz_layer, tv_layer;
+  int owner_idx[kMaxGroup], x_row[kMaxGroup], v_row[kMaxGroup], y_row[kMaxGroup], tail_pos[kMaxGroup];
+};
+struct LowRankWrite {
+  int n, d_model, d_ff, rank, C;
+  void *slots;
+  long long slot_elems, layer_off;
+  const int *sel;
+  const void *tailZ;
+  long long tz_owner, tz_layer;
+  float eta;
+  int *fail_flag;
+  int owner_idx[kMaxGroup];
+};
+cudaError_t launch_lowrank_read(const LowRankRead &p, const ChunkLaunch &base, cudaStream_t s);
+cudaError_t launch_lowrank_write(const LowRankWrite &p, cudaStream_t s);
 
 int device_sm_count();
 bool read_chunk_supported(int d_model, int d_ff, int C);

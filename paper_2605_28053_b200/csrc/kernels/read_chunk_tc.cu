@@ -36,6 +36,9 @@ struct ChunkParams {
   void *Y;
   void *tailZ, *tailV;
   long long tz_owner, tv_owner, tz_layer, tv_layer;
+  int delta, append, valid_rows, ksplit;
+  float *Y32;
+  long long y32_slab;
   int owner_idx[kMaxGroup];
 };
 
@@ -53,8 +56,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(t_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nt = p.d_model / BN, nk = p.d_ff / BK;
-  const int n_tiles = p.n * nt;
+  const int nt = p.d_model / BN, nk_all = p.d_ff / BK, KS = p.ksplit;
+  const int n_tiles = p.n * nt * KS;
+  // tile u -> (member / row block b, N block j, K range ks)
+  auto decode = [&](int u, int &b, int &j, int &kb0, int &kb1) {
+    const int ks = u % KS, bj = u / KS;
+    b = bj / nt;
+    j = bj - b * nt;
+    kb0 = nk_all * ks / KS;
+    kb1 = nk_all * (ks + 1) / KS;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -78,17 +89,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch(&tmD);
       int it = 0;
       for (int u = blockIdx.x; u < n_tiles; u += gridDim.x) {
-        const int b = u / nt, j = u - b * nt;
-        const int o = p.owner_idx[b];
-        const int slot_l = (2 * o + p.sel[o]) * p.L + p.layer;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        int b, j, kb0, kb1;
+        decode(u, b, j, kb0, kb1);
+        const int o = p.delta ? p.owner_idx[b] : 0;
+        const int slot_l = p.delta ? (2 * o + p.sel[o]) * p.L + p.layer : 0;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % kStages;
           if (it >= kStages) mbar_wait(empty + s, ((it / kStages) - 1) & 1);
           unsigned char *st = smem + s * STAGE;
-          mbar_expect_tx(full + s, STAGE);
+          mbar_expect_tx(full + s, p.delta ? STAGE : A_BYTES + B_BYTES);
           tma_load_3d(st, &tmX, full + s, kb * BK, 0, b);
           tma_load_3d(st + A_BYTES, &tmW, full + s, kb * BK, j * BN, p.layer);
-          tma_load_3d(st + A_BYTES + B_BYTES, &tmD, full + s, kb * BK, j * BN, slot_l);
+          if (p.delta) tma_load_3d(st + A_BYTES + B_BYTES, &tmD, full + s, kb * BK, j * BN, slot_l);
         }
       }
     }
@@ -96,9 +108,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc = idesc_bf16(BM, BN, 0, 0);
     int it = 0, k = 0;
     for (int u = blockIdx.x; u < n_tiles; u += gridDim.x, ++k) {
+      int b, j, kb0, kb1;
+      decode(u, b, j, kb0, kb1);
       if (k > 0) mbar_wait(t_empty, (k - 1) & 1);
       tc_fence_after();
-      for (int kb = 0; kb < nk; ++kb, ++it) {
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
         const int s = it % kStages;
         mbar_wait(full + s, (it / kStages) & 1);
         tc_fence_after();
@@ -108,11 +122,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {        // K=16 step = 32 bytes inside the 128 B swizzle row
             const u64 ad = smem_desc_sw128(a0 + kk * 32, 16, 1024);
-            mma_bf16(tmem, ad, smem_desc_sw128(w0 + kk * 32, 16, 1024), idesc, (kb | kk) ? 1u : 0u);
-            mma_bf16(tmem, ad, smem_desc_sw128(d0 + kk * 32, 16, 1024), idesc, 1u);
+            mma_bf16(tmem, ad, smem_desc_sw128(w0 + kk * 32, 16, 1024), idesc, ((kb - kb0) | kk) ? 1u : 0u);
+            if (p.delta) mma_bf16(tmem, ad, smem_desc_sw128(d0 + kk * 32, 16, 1024), idesc, 1u);
           }
           mma_commit(empty + s);
-          if (kb == nk - 1) mma_commit(t_full);
+          if (kb == kb1 - 1) mma_commit(t_full);
         }
         __syncwarp();
       }
@@ -122,8 +136,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int et = threadIdx.x - 64;
     int k = 0;
     for (int u = blockIdx.x; u < n_tiles; u += gridDim.x, ++k) {
-      const int b = u / nt, j = u - b * nt;
-      {                                                      // a4: tile j appends slice j of the chunk to the tail
+      int b, j, kb0, kb1;
+      decode(u, b, j, kb0, kb1);
+      const int ks = u % KS;
+      if (p.append) {                                        // a4: tile j appends slice j of the chunk to the tail
         const int o = p.owner_idx[b];
         auto copy_slice = [&](const uint4 *src, uint4 *dst, size_t total) {
           const size_t lo = total * j / nt, hi = total * (j + 1) / nt;
@@ -144,11 +160,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(t_full, k & 1);
       tc_fence_after();
       __nv_bfloat16 *yrow = static_cast<__nv_bfloat16 *>(p.Y) + ((size_t)b * p.C + row) * p.d_model + j * BN;
+      float *yrow32 = p.Y32 ? p.Y32 + ks * p.y32_slab + ((size_t)b * p.C + row) * p.d_model + j * BN : nullptr;
+      const bool valid = row < p.C && (!p.Y32 || b * p.C + row < p.valid_rows);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
-        if (row < p.C) {
+        if (valid && yrow32) {
+          float4 *d4 = reinterpret_cast<float4 *>(yrow32 + c * 32);
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            d4[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]), __uint_as_float(r[4 * v + 2]),
+                                __uint_as_float(r[4 * v + 3]));
+        } else if (valid) {
           uint32_t o16[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
@@ -186,7 +210,7 @@ cudaError_t launch_bn(const CUtensorMap &mX, const CUtensorMap &mW, const CUtens
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int tiles = p.n * (p.d_model / BN);
+  const int tiles = p.n * (p.d_model / BN) * p.ksplit;
   read_chunk_tc_kernel<BN><<<std::min(device_sm_count(), tiles), kThreads, smem, s>>>(mX, mW, mD, p);
   count_launch();
   return cudaGetLastError();
@@ -223,16 +247,24 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
   p.tv_owner = cl.tv_owner;
   p.tz_layer = cl.tz_layer;
   p.tv_layer = cl.tv_layer;
+  p.delta = cl.delta;
+  p.append = cl.append;
+  p.valid_rows = cl.valid_rows;
+  p.Y32 = cl.Y32;
+  p.ksplit = cl.ksplit < 1 ? 1 : cl.ksplit;
+  p.y32_slab = cl.y32_slab;
   for (int b = 0; b < cl.n; ++b) p.owner_idx[b] = cl.owner_idx[b];
   const int sms = device_sm_count();
   const bool can160 = cl.d_model % 160 == 0, can128 = cl.d_model % 128 == 0;
   const bool use160 =
-      can160 && (!can128 || wave_eff(cl.n * (cl.d_model / 160), sms) >= wave_eff(cl.n * (cl.d_model / 128), sms));
+      can160 && (!can128 || wave_eff(cl.n * (cl.d_model / 160) * std::max(1, cl.ksplit), sms) >=
+                                 wave_eff(cl.n * (cl.d_model / 128) * std::max(1, cl.ksplit), sms));
   const int BN = use160 ? 160 : 128;
   CUtensorMap mX, mW, mD;
   if (!ptx::make_map_bf16_3d(&mX, cl.X, cl.d_ff, cl.C, cl.n, BK, BM) ||
       !ptx::make_map_bf16_3d(&mW, cl.w_down, cl.d_ff, cl.d_model, cl.L, BK, BN) ||
-      !ptx::make_map_bf16_3d(&mD, cl.slots, cl.d_ff, cl.d_model, (uint64_t)cl.max_slots * cl.L, BK, BN))
+      !ptx::make_map_bf16_3d(&mD, cl.delta ? cl.slots : cl.w_down, cl.d_ff, cl.d_model,
+                             cl.delta ? (uint64_t)cl.max_slots * cl.L : (uint64_t)cl.L, BK, BN))
     return cudaErrorInvalidValue;
   return use160 ? launch_bn<160>(mX, mW, mD, p, s) : launch_bn<128>(mX, mW, mD, p, s);
 }

@@ -28,7 +28,8 @@ struct OwnerRec {
 };
 
 struct Layout {
-  size_t slots = 0, tailZ = 0, tailV = 0, sel = 0, ver = 0, flags = 0, P = 0, tickets = 0, total = 0;
+  size_t slots = 0, tailZ = 0, tailV = 0, sel = 0, ver = 0, flags = 0, P = 0, tickets = 0;
+  size_t Xg = 0, Y32 = 0, U = 0, total = 0;      // low-rank READ workspace
 };
 
 Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt);
@@ -43,7 +44,7 @@ struct ttt_pool {
   size_t arena_bytes = 0;
   const void *w_down = nullptr;
   size_t esize = 4;
-  long long E = 0, slot_elems = 0, tz_owner = 0, tv_owner = 0;
+  long long E = 0, Ew = 0, slot_elems = 0, tz_owner = 0, tv_owner = 0;   // E: payload / layer, Ew: W_down / layer
   ttt::Layout lay;
   std::unordered_map<uint64_t, ttt::OwnerRec> owners;
   std::vector<int> free_idx, free_ckpt;

@@ -50,9 +50,13 @@ static ttt_status cuda_fail(cudaError_t e, const char *what) {
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+size_t payload_elems(const ttt_shape &s) {
+  return s.backend == TTT_LOW_RANK ? (size_t)s.rank * (s.d_ff + s.d_model) : (size_t)s.d_model * s.d_ff;
+}
+
 Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt) {
   const size_t es = s.dtype == TTT_BF16 ? 2 : 4;
-  const size_t E = (size_t)s.d_model * s.d_ff;
+  const size_t E = payload_elems(s);
   const size_t slot = (size_t)s.n_layers * E * es;
   Layout L;
   size_t off = 0;
@@ -64,13 +68,23 @@ Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt) {
   L.flags = off;   off = align_up(off + 64, 256);
   L.P = off;       off = align_up(off + 2 * (size_t)kMaxReadMembers * s.d_model * 4, 256);
   L.tickets = off; off = align_up(off + (size_t)s.d_model * 4, 1024);
+  if (s.backend == TTT_LOW_RANK) {
+    const size_t rows = align_up((size_t)max_owners, 128);
+    L.Xg = off;  off = align_up(off + rows * s.d_ff * es, 1024);
+    L.Y32 = off; off = align_up(off + (size_t)kMaxKSplit * rows * s.d_model * 4, 1024);
+    L.U = off;   off = align_up(off + (size_t)max_owners * 64 * 4, 1024);
+  }
   L.total = off;
   return L;
 }
 
 static ttt_status check_shape(const ttt_shape *s) {
   if (!s) return fail(TTT_E_INVALID_ARG, "null shape");
-  if (s->backend != TTT_FAST_WEIGHT) return fail(TTT_E_SHAPE, "only the fast-weight backend (τ=0) is built");
+  if (s->backend != TTT_FAST_WEIGHT && s->backend != TTT_LOW_RANK)
+    return fail(TTT_E_SHAPE, "backend must be fast-weight (τ=0) or low-rank (τ=1)");
+  if (s->backend == TTT_LOW_RANK &&
+      (s->rank < 1 || s->rank > 64 || s->dtype != TTT_BF16 || !read_chunk_supported(s->d_model, s->d_ff, 128)))
+    return fail(TTT_E_SHAPE, "low-rank: rank in [1,64], bf16, d_ff % 64 == 0, d_model % 128 (or 160) == 0");
   if (s->dtype != TTT_BF16 && s->dtype != TTT_FP32) return fail(TTT_E_SHAPE, "dtype");
   if (s->d_model <= 0 || s->d_ff <= 0 || s->chunk <= 0 || s->n_layers <= 0)
     return fail(TTT_E_SHAPE, "non-positive dimension");
@@ -201,7 +215,8 @@ ttt_status tttstate_pool_create(const ttt_shape *shape, int32_t shape_id, int32_
   p->arena_bytes = arena_bytes;
   p->w_down = w_down;
   p->esize = shape->dtype == TTT_BF16 ? 2 : 4;
-  p->E = (long long)shape->d_model * shape->d_ff;
+  p->E = (long long)payload_elems(*shape);
+  p->Ew = (long long)shape->d_model * shape->d_ff;
   p->slot_elems = p->E * shape->n_layers;
   p->tz_owner = (long long)shape->n_layers * shape->chunk * shape->d_ff;
   p->tv_owner = (long long)shape->n_layers * shape->chunk * shape->d_model;
@@ -351,7 +366,8 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
   }
   // f3: with C = 1 every step is a WRITE whose evidence is this token only, so the
   // candidate is written here, in the same pass over ΔW (write_commit then only commits).
-  const bool fuse = g->effect == TTT_WRITE && sh.chunk == 1 && g_write_impl.load() != 1;
+  const bool fuse = g->effect == TTT_WRITE && sh.chunk == 1 && sh.backend == TTT_FAST_WEIGHT &&
+                    g_write_impl.load() != 1;
   int need_evict = 0;
   if (fuse)
     for (int b = 0; b < g->n; ++b) need_evict += (recs[b]->n_applied == 0 && pinned_in_shadow(*recs[b]));
@@ -362,6 +378,48 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
   if (fuse)
     for (int b = 0; b < g->n; ++b)
       if (recs[b]->n_applied == 0 && pinned_in_shadow(*recs[b])) CUDA_TRY(evict_pinned(p, *recs[b], s));
+  if (sh.backend == TTT_LOW_RANK) {                 // NEXT f1: u = A x, base GEMM, y = base + Bᵀu
+    LowRankRead lp{};
+    lp.n = g->n; lp.d_model = sh.d_model; lp.d_ff = sh.d_ff; lp.rank = sh.rank;
+    lp.X = X; lp.Vt = Vt; lp.resid = resid; lp.Y = Y;
+    lp.Xg = p->arena + p->lay.Xg;
+    lp.Y32 = reinterpret_cast<float *>(p->arena + p->lay.Y32);
+    lp.u = reinterpret_cast<float *>(p->arena + p->lay.U);
+    lp.slots = p->arena + p->lay.slots;
+    lp.slot_elems = p->slot_elems;
+    lp.layer_off = (long long)layer * p->E;
+    lp.sel = p->d_sel();
+    lp.tailZ = p->arena + p->lay.tailZ;
+    lp.tailV = p->arena + p->lay.tailV;
+    lp.tz_owner = p->tz_owner; lp.tv_owner = p->tv_owner;
+    lp.tz_layer = (long long)layer * sh.chunk * sh.d_ff;
+    lp.tv_layer = (long long)layer * sh.chunk * sh.d_model;
+    for (int b = 0; b < g->n; ++b) {
+      lp.owner_idx[b] = recs[b]->idx;
+      lp.x_row[b] = x_rows ? x_rows[b] : b;
+      lp.v_row[b] = v_rows ? v_rows[b] : b;
+      lp.y_row[b] = y_rows ? y_rows[b] : b;
+      lp.tail_pos[b] = recs[b]->tail_len;
+    }
+    ChunkLaunch cl{};
+    cl.n = (g->n + 127) / 128; cl.d_model = sh.d_model; cl.d_ff = sh.d_ff; cl.C = 128; cl.L = sh.n_layers;
+    cl.layer = layer; cl.max_slots = 1; cl.sel = p->d_sel();
+    cl.X = lp.Xg; cl.w_down = p->w_down; cl.slots = p->w_down;
+    cl.delta = 0; cl.append = 0; cl.Y32 = lp.Y32; cl.valid_rows = g->n;
+    // split K so the base GEMM (one or two 128-row blocks) covers the SMs; slabs summed in order
+    const int ntile = cl.n * (sh.d_model % 160 == 0 ? sh.d_model / 160 : sh.d_model / 128);
+    cl.ksplit = std::max(1, std::min({kMaxKSplit, device_sm_count() / ntile, sh.d_ff / 64}));
+    cl.y32_slab = (long long)align_up((size_t)p->max_owners, 128) * sh.d_model;
+    lp.ksplit = cl.ksplit;
+    lp.y32_slab = cl.y32_slab;
+    cudaError_t e = launch_lowrank_read(lp, cl, s);
+    if (e != cudaSuccess) return cuda_fail(e, "low-rank READ");
+    for (int b = 0; b < g->n; ++b) {
+      recs[b]->applied[layer] = 1;
+      recs[b]->n_applied += 1;
+    }
+    return TTT_OK;
+  }
   int per = std::min(kMaxReadMembers, g->n);
   while (per > 1 && !read_decode_fits(per, sh.d_model, sh.d_ff, (int)p->esize)) --per;
   if (!read_decode_fits(per, sh.d_model, sh.d_ff, (int)p->esize))
@@ -369,7 +427,7 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
   for (int b0 = 0; b0 < g->n; b0 += per) {
     ReadParams rp{};
     rp.X = X; rp.Vt = Vt; rp.resid = resid; rp.Y = Y;
-    rp.w_down_l = static_cast<const unsigned char *>(p->w_down) + (size_t)layer * p->E * p->esize;
+    rp.w_down_l = static_cast<const unsigned char *>(p->w_down) + (size_t)layer * p->Ew * p->esize;
     rp.slots = p->arena + p->lay.slots;
     rp.slot_elems = p->slot_elems;
     rp.layer_off = (long long)layer * p->E;
@@ -435,7 +493,7 @@ ttt_status read_apply_chunk(ttt_pool *p, const ttt_group *g, int32_t layer, cons
   const ttt_shape &sh = p->sh;
   if (g->effect != TTT_WRITE) return fail(TTT_E_WRONG_EFFECT, "a whole chunk ends in its boundary WRITE");
   if (layer < 0 || layer >= sh.n_layers) return fail(TTT_E_SHAPE, "layer out of range");
-  if (sh.dtype != TTT_BF16 || !read_chunk_supported(sh.d_model, sh.d_ff, sh.chunk))
+  if (sh.backend != TTT_FAST_WEIGHT || sh.dtype != TTT_BF16 || !read_chunk_supported(sh.d_model, sh.d_ff, sh.chunk))
     return fail(TTT_E_SHAPE, "chunk READ needs bf16, d_ff % 64 == 0, d_model % 128 (or 160) == 0, C <= 128");
   for (int b = 0; b < g->n; ++b) {
     OwnerRec &r = *recs[b];
@@ -499,7 +557,26 @@ ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32
     for (int b = 0; b < g->n; ++b) forced |= (fail_mask[b / 32] >> (b % 32)) & 1u;
   if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (!fused) {
+  if (!fused && sh.backend == TTT_LOW_RANK) {
+    for (int b = 0; b < g->n; ++b)
+      if (pinned_in_shadow(*recs[b])) CUDA_TRY(evict_pinned(p, *recs[b], s));
+    LowRankWrite lw{};
+    lw.n = g->n; lw.d_model = sh.d_model; lw.d_ff = sh.d_ff; lw.rank = sh.rank; lw.C = sh.chunk;
+    lw.slots = p->arena + p->lay.slots;
+    lw.slot_elems = p->slot_elems;
+    lw.sel = p->d_sel();
+    lw.tailZ = p->arena + p->lay.tailZ;
+    lw.tz_owner = p->tz_owner;
+    lw.eta = eta;
+    lw.fail_flag = p->d_fail_flag();
+    for (int b = 0; b < g->n; ++b) lw.owner_idx[b] = recs[b]->idx;
+    for (int l = 0; l < sh.n_layers; ++l) {
+      lw.layer_off = (long long)l * p->E;
+      lw.tz_layer = (long long)l * sh.chunk * sh.d_ff;
+      cudaError_t e = launch_lowrank_write(lw, s);
+      if (e != cudaSuccess) return cuda_fail(e, "low-rank write launch");
+    }
+  } else if (!fused) {
     for (int b = 0; b < g->n; ++b)                  // preserve pinned checkpoints sitting in the shadow slot
       if (pinned_in_shadow(*recs[b])) CUDA_TRY(evict_pinned(p, *recs[b], s));
     WriteParams wp{};

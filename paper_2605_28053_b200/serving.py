@@ -25,13 +25,15 @@ class Engine:
 
     def __init__(self, d_model: int, d_ff: int, chunk: int, n_layers: int, dtype: str, max_owners: int,
                  w_down: torch.Tensor, n_ckpt: int = 0, mode: int = capi.MODE_FULL, B: int = 8, w: int = 0,
-                 shape_id: int = 0, placement: int = 0, device=None, eta: float = 0.01):
+                 shape_id: int = 0, placement: int = 0, device=None, eta: float = 0.01,
+                 backend: int = capi.FAST_WEIGHT, rank: int = 0):
         device = torch.device(device) if device is not None else w_down.device
         assert w_down.is_cuda, "w_down must be a device tensor"
         self.d_model, self.d_ff, self.chunk, self.n_layers, self.dtype = d_model, d_ff, chunk, n_layers, dtype
         self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float32
         self.eta = float(torch.tensor(eta, dtype=torch.float32))
-        self.shape = capi.make_shape(d_model, d_ff, chunk, n_layers, dtype)
+        self.shape = capi.make_shape(d_model, d_ff, chunk, n_layers, dtype, backend=backend, rank=rank)
+        self.backend, self.rank = backend, rank
         self.arena_bytes = capi.tttstate_pool_bytes(self.shape, max_owners, n_ckpt)
         self._arena = torch.empty(self.arena_bytes + 1024, dtype=torch.uint8, device=device)
         base = (self._arena.data_ptr() + 1023) // 1024 * 1024
@@ -66,6 +68,7 @@ class RunLog:
     versions: dict = field(default_factory=dict)
     fallbacks: int = 0
     device_failures: int = 0
+    branches: dict = field(default_factory=dict)    # live branch owner -> version
 
 
 class InputSource:
@@ -104,6 +107,8 @@ class Server:
         self.pending: set = set()
         self.ready_at: dict = {}
         self.failed_once: set = set()
+        self.forks: dict = {}
+        self.branches: set = set()
         self.clock = 0
         self.read_events: list = []       # (start, end) CUDA event pairs around read_apply
         self.write_events: list = []      # (start, end) around write_commit
@@ -137,6 +142,15 @@ class Server:
                         vb = capi.tttstate_version(pool, owners[s])
                         va = capi.rollback(pool, owners[s], stream)
                         log.commits.append((s, self.pos[s], vb, va, "rolled_back"))
+                    elif op == "fork":                                  # new lineage
+                        k = self.forks.get(s, 0)
+                        capi.tttstate_fork(pool, owners[s], tr.branch_owner(s, k), stream)
+                        self.branches.add(tr.branch_owner(s, k))
+                        self.forks[s] = k + 1
+                    elif op == "release":
+                        b = tr.branch_owner(s, self.forks[s] - 1)
+                        capi.tttstate_free(pool, b)
+                        self.branches.discard(b)
                 events.append(capi.tttstate_next_event(pool, owners[s], clock))
                 self.pending.add(s)
                 self.ready_at[s] = clock
@@ -201,6 +215,8 @@ class Server:
     def finish(self) -> RunLog:
         for s, o in enumerate(self.owners):
             self.log.versions[s] = capi.tttstate_version(self.eng.pool, o)
+        for b in self.branches:
+            self.log.branches[b] = capi.tttstate_version(self.eng.pool, b)
         return self.log
 
 

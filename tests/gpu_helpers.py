@@ -35,6 +35,9 @@ class HostGenInputs(InputSource):
     def init_delta(self, s):
         if self.tr.delta0 == "zero":
             return None
+        if self.tr.backend == 1:                 # low-rank payload per layer: A (R·d_ff) then B (R·d_model)
+            flat = [np.concatenate([a.ravel(), b.ravel()]) for a, b in (self.tr.delta0_of(s, l) for l in self.layers)]
+            return to_dev(np.stack(flat), self.tr.dtype, self.dev)
         return to_dev(np.stack([self.tr.delta0_of(s, l) for l in self.layers]), self.tr.dtype, self.dev)
 
     def tail_prefill(self, s):
@@ -64,7 +67,16 @@ def make_engine(tr, device="cuda", n_ckpt=4, max_owners=None, mode=None, B=None,
     return Engine(tr.d_model, tr.d_ff, tr.chunk, tr.n_layers, tr.dtype,
                   max_owners or tr.n_streams + 2, W, n_ckpt=n_ckpt,
                   mode=tr.mode if mode is None else mode, B=tr.B if B is None else B,
-                  w=tr.w if w is None else w, eta=tr.eta)
+                  w=tr.w if w is None else w, eta=tr.eta, backend=tr.backend, rank=tr.rank)
+
+
+def read_lowrank(eng, tr, owner, l):
+    """Committed (A, B) of one owner-layer as float64 (low-rank backend)."""
+    from paper_2605_28053_b200 import capi
+    flat = capi.tttstate_read_payload_flat(eng.pool, owner, l, tr.rank * (tr.d_ff + tr.d_model), tr.dtype)
+    A = nm.widen(flat[: tr.rank * tr.d_ff], tr.dtype).reshape(tr.rank, tr.d_ff)
+    B = nm.widen(flat[tr.rank * tr.d_ff:], tr.dtype).reshape(tr.rank, tr.d_model)
+    return A, B
 
 
 class DeviceGenInputs(InputSource):

@@ -1,0 +1,46 @@
+"""NEXT f1 parity: low-rank delta TTTState + speculative branch lineages (BJ configs[3]
+structure at reduced dims) — READ (u = A x, tcgen05 base GEMM with split-K, y = base + Bᵀu),
+WRITE (A' = A + η(A m)mᵀ, B' = B), fork / release / snapshot / rollback."""
+import pytest
+import torch
+
+from oracle import numerics as nm
+from oracle.run import run_batched
+from workload import traces as T
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2605_28053_b200.serving import run_trace  # noqa: E402
+
+from .gpu_helpers import HostGenInputs, make_engine, read_lowrank  # noqa: E402
+
+DEV = "cuda"
+
+
+@pytest.mark.parametrize("rank,streams,d_model,d_ff", [(8, 16, 256, 384), (16, 130, 320, 256), (64, 4, 256, 448)])
+def test_config4_lowrank_branches_parity(rank, streams, d_model, d_ff):
+    tr = T.config4_lowrank(n_steps=26, n_layers=2, rank=rank, d_model=d_model, d_ff=d_ff, chunk=8,
+                           n_streams=streams, seed=rank)
+    tr = tr.replace(B=min(streams, 256))
+    ref = run_batched(tr)
+    eng = make_engine(tr, DEV, n_ckpt=streams + 2, max_owners=2 * streams + 2)
+    src = HostGenInputs(tr, DEV)
+    log = run_trace(eng, tr, src)
+    torch.cuda.synchronize()
+    tol = nm.TOL["bf16"]
+    worst = max(nm.normwise_rel_err(src.out[k], ref.outputs[k]) for k in ref.outputs)
+    assert worst <= tol, worst
+    assert log.versions == ref.versions and log.commits == ref.commits and log.plan == ref.plan
+    assert log.branches == {b: v for b, (v, _) in ref.branches.items()}
+    for s in range(min(streams, 6)):
+        for l in range(tr.n_layers):
+            A, B = read_lowrank(eng, tr, tr.owner(s), l)
+            rA, rB = ref.state[s][l]
+            assert nm.normwise_rel_err(A, rA) <= tol and nm.normwise_rel_err(B, rB) == 0.0
+    for b, (v, S) in list(ref.branches.items())[:4]:           # fork isolation: branch bytes = source at fork
+        for l in range(tr.n_layers):
+            A, B = read_lowrank(eng, tr, b, l)
+            assert nm.normwise_rel_err(A, S[l][0]) <= tol and nm.normwise_rel_err(B, S[l][1]) == 0.0
