@@ -144,6 +144,30 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
   const int nvec = dff / E::kVec;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+  // Programmatic dependent launch (PDL): let the next layer's READ grid be scheduled as our
+  // CTAs retire, and overlap our own launch with the previous kernel's tail.  Before
+  // griddepcontrol.wait only W_down is touched — no kernel ever writes it — so warps whose
+  // first task is a base row issue their first batch early; everything that may depend on
+  // earlier kernels in the stream (x, the active-slot table, ΔW, the workspace) waits.
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int n_tasks = (n + 1) * dm;
+  const int stride = gridDim.x * kWarps;
+  int t = blockIdx.x * kWarps + warp;
+  auto load = [&](uint4 (&buf)[kU], const uint4 *row, int v0) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (v0 + 32 * u < nvec) buf[u] = ld_stream(row + v0 + 32 * u);
+  };
+  uint4 cur[kU], nxt[kU];
+  int v = lane;
+  const uint4 *row = nullptr;
+  const bool early = t < dm;                        // first task is a W_down row
+  if (early) {
+    row = static_cast<const uint4 *>(p.w_down_l) + (size_t)t * nvec;
+    load(cur, row, v);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
   if (tid <= n) {
     if (tid == 0) {
       s_row0[0] = static_cast<const uint4 *>(p.w_down_l);
@@ -157,42 +181,38 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
                                                     (2LL * o + 1 - p.sel[o]) * p.slot_elems + p.layer_off);
     }
   }
-  for (int idx = tid; idx < n * nvec; idx += kThreads) {
-    const int b = idx / nvec, v = idx - b * nvec;
-    xs[idx] = reinterpret_cast<const uint4 *>(static_cast<const T *>(p.X) + (size_t)p.x_row[b] * dff)[v];
-  }
-  __syncthreads();
-
-  // a4 — TailBufferUpdate: CTA b appends member b's (z, v) at its tail index.
-  if (blockIdx.x < n) {
-    const int b = blockIdx.x, o = p.owner_idx[b];
-    uint4 *tz = reinterpret_cast<uint4 *>(static_cast<T *>(p.tailZ) + o * p.tz_owner + p.tz_layer +
-                                          (size_t)p.tail_pos[b] * dff);
-    for (int v = tid; v < nvec; v += kThreads) tz[v] = xs[b * nvec + v];
-    T *tv = static_cast<T *>(p.tailV) + o * p.tv_owner + p.tv_layer + (size_t)p.tail_pos[b] * dm;
-    const T *src = static_cast<const T *>(p.Vt) + (size_t)p.v_row[b] * dm;
-    for (int i = tid; i < dm; i += kThreads) tv[i] = src[i];
-  }
-
-  const int n_tasks = (n + 1) * dm;
-  const int stride = gridDim.x * kWarps;
-  int t = blockIdx.x * kWarps + warp;
-  if (t >= n_tasks) return;
+  __syncthreads();                                 // row-0 table ready
 
   auto row_of = [&](int task) {
     const int m = task / dm;
     return s_row0[m] + (size_t)(task - m * dm) * nvec;
   };
-  auto load = [&](uint4 (&buf)[kU], const uint4 *row, int v0) {
-#pragma unroll
-    for (int u = 0; u < kU; ++u)
-      if (v0 + 32 * u < nvec) buf[u] = ld_stream(row + v0 + 32 * u);
-  };
+  if (!early && t < n_tasks) {
+    row = row_of(t);
+    load(cur, row, v);
+  }
 
-  uint4 cur[kU], nxt[kU];
-  const uint4 *row = row_of(t);
-  int v = lane;
-  load(cur, row, v);
+  for (int idx = tid; idx < n * nvec; idx += kThreads) {
+    const int b = idx / nvec, vv = idx - b * nvec;
+    xs[idx] = reinterpret_cast<const uint4 *>(static_cast<const T *>(p.X) + (size_t)p.x_row[b] * dff)[vv];
+  }
+  // a4 — TailBufferUpdate, spread over every CTA: z rows as 16-byte vectors, v rows as elements.
+  {
+    const int zq = n * nvec, gtid = blockIdx.x * kThreads + tid, gsz = gridDim.x * kThreads;
+    for (int idx = gtid; idx < zq; idx += gsz) {
+      const int b = idx / nvec, vv = idx - b * nvec, o = p.owner_idx[b];
+      reinterpret_cast<uint4 *>(static_cast<T *>(p.tailZ) + o * p.tz_owner + p.tz_layer +
+                                (size_t)p.tail_pos[b] * dff)[vv] =
+          reinterpret_cast<const uint4 *>(static_cast<const T *>(p.X) + (size_t)p.x_row[b] * dff)[vv];
+    }
+    for (int idx = gtid; idx < n * dm; idx += gsz) {
+      const int b = idx / dm, i = idx - b * dm, o = p.owner_idx[b];
+      (static_cast<T *>(p.tailV) + o * p.tv_owner + p.tv_layer + (size_t)p.tail_pos[b] * dm)[i] =
+          (static_cast<const T *>(p.Vt) + (size_t)p.v_row[b] * dm)[i];
+    }
+  }
+  __syncthreads();
+  if (t >= n_tasks) return;
   Acc acc[kMaxReadMembers];
 #pragma unroll
   for (int r = 0; r < kMaxReadMembers; ++r) acc[r] = E::zero();
@@ -301,9 +321,20 @@ cudaError_t launch_cfg1(const ReadParams &p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured = (int)smem;
   }
-  read_decode_kernel<T, TH, U, FUSE><<<device_sm_count(), TH, smem, s>>>(p);
+  static const bool pdl = !getenv("TTT_PDL") || atoi(getenv("TTT_PDL")) != 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(device_sm_count());
+  cfg.blockDim = dim3(TH);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, read_decode_kernel<T, TH, U, FUSE>, p);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <typename T, int TH, int U>
