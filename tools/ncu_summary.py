@@ -42,6 +42,7 @@ def raw(rep):
 
 def summarise(rep, label, outdir):
     res = {}
+    all_lines = []
     for d, u in raw(rep):
         lines = [f"# {label}: {d.get('Kernel Name', '?')}", f"# source: {os.path.basename(rep)} (ncu --set full, 1 launch)"]
         for k in KEYS:
@@ -54,9 +55,10 @@ def summarise(rep, label, outdir):
         t_ns = float(d["gpu__time_duration.sum"]) * (1e3 if u["gpu__time_duration.sum"] == "us" else 1)
         lines.append(f"# dram traffic per launch = {rdb + wrb:.4e} B; achieved {(rdb + wrb) / t_ns:.1f} GB/s "
                      f"(cold-cache, serialised replay)")
-        open(os.path.join(outdir, f"{label}_ncu.txt"), "w").write("\n".join(lines) + "\n")
+        all_lines += lines + [""]
         res = {"dram_bytes_per_launch": rdb + wrb, "dram_read": rdb, "dram_write": wrb, "time_ns": t_ns,
                "source": os.path.relpath(os.path.join(outdir, f"{label}_ncu.txt"), ROOT)}
+    open(os.path.join(outdir, f"{label}_ncu.txt"), "w").write("\n".join(all_lines))
     return res
 
 
@@ -93,6 +95,7 @@ def main():
     ap.add_argument("--write")
     ap.add_argument("--launches")
     ap.add_argument("--chunk")
+    ap.add_argument("--extra", action="append", default=[], help="label=path.ncu-rep")
     a = ap.parse_args()
     outdir = os.path.join(ROOT, "profiles", a.round)
     os.makedirs(outdir, exist_ok=True)
@@ -103,6 +106,9 @@ def main():
         traffic["write_tc_kernel"] = summarise(a.write, "write_tc", outdir)
     if a.chunk:
         traffic["read_chunk_tc_kernel"] = summarise(a.chunk, "read_chunk_tc", outdir)
+    for e in a.extra:
+        label, path = e.split("=", 1)
+        summarise(path, label, outdir)
     if a.launches:
         shutil.copy(a.launches, os.path.join(outdir, "launches.csv"))
         shares(a.launches, outdir)
