@@ -22,41 +22,65 @@ namespace {
 
 __device__ __forceinline__ float bf(const __nv_bfloat16 v) { return __bfloat162float(v); }
 
-// one warp per (member b, rank row k)
-__global__ void __launch_bounds__(256) lr_u_kernel(const LowRankRead p) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int R = p.rank, dff = p.d_ff, dm = p.d_model;
-  const int b = warp / R, k = warp - b * R;
-  if (b >= p.n) return;
+// one CTA per member b: x_b staged in shared memory once, warps over the rank rows k,
+// 4 independent 16-byte loads of A in flight per lane.
+constexpr int kUThreads = 1024;                   // 32 warps = 32 rank rows per CTA
+__global__ void __launch_bounds__(kUThreads) lr_u_kernel(const LowRankRead p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint4 *xs = reinterpret_cast<uint4 *>(smem);
+  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int R = p.rank, dff = p.d_ff, dm = p.d_model, nvec = dff / 8;
+  const bool first = blockIdx.y == 0;              // rank block 0 also gathers x and appends the tail
   const int o = p.owner_idx[b];
-  const __nv_bfloat16 *x = static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff;
-  const __nv_bfloat16 *slot = static_cast<const __nv_bfloat16 *>(p.slots) +
-                              (2LL * o + p.sel[o]) * p.slot_elems + p.layer_off;
-  const __nv_bfloat16 *A = slot + (size_t)k * dff;
-  const uint4 *a4 = reinterpret_cast<const uint4 *>(A), *x4 = reinterpret_cast<const uint4 *>(x);
-  float acc = 0.f;
-  for (int v = lane; v < dff / 8; v += 32) {
-    const uint4 a = a4[v], z = x4[v];
-    const __nv_bfloat16 *ah = reinterpret_cast<const __nv_bfloat16 *>(&a);
-    const __nv_bfloat16 *zh = reinterpret_cast<const __nv_bfloat16 *>(&z);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc = fmaf(bf(ah[e]), bf(zh[e]), acc);
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) p.u[(size_t)b * 64 + k] = acc;
-  if (k == 0) {                                    // gather x_b for the base GEMM; tail append (a4)
-    uint4 *xg = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.Xg) + (size_t)b * dff);
-    uint4 *tz = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.tailZ) + o * p.tz_owner + p.tz_layer +
-                                          (size_t)p.tail_pos[b] * dff);
-    for (int v = lane; v < dff / 8; v += 32) {
-      const uint4 z = x4[v];
+  const uint4 *x4 = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff);
+  uint4 *xg = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.Xg) + (size_t)b * dff);
+  uint4 *tz = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.tailZ) + o * p.tz_owner + p.tz_layer +
+                                        (size_t)p.tail_pos[b] * dff);
+  for (int v = tid; v < nvec; v += kUThreads) {     // stage x; gather for the base GEMM; tail append (a4)
+    const uint4 z = x4[v];
+    xs[v] = z;
+    if (first) {
       xg[v] = z;
       tz[v] = z;
     }
+  }
+  if (first) {
     const __nv_bfloat16 *vt = static_cast<const __nv_bfloat16 *>(p.Vt) + (size_t)p.v_row[b] * dm;
     __nv_bfloat16 *tv = static_cast<__nv_bfloat16 *>(p.tailV) + o * p.tv_owner + p.tv_layer + (size_t)p.tail_pos[b] * dm;
-    for (int i = lane; i < dm; i += 32) tv[i] = vt[i];
+    for (int i = tid; i < dm; i += kUThreads) tv[i] = vt[i];
+  }
+  __syncthreads();
+  const __nv_bfloat16 *slot = static_cast<const __nv_bfloat16 *>(p.slots) +
+                              (2LL * o + p.sel[o]) * p.slot_elems + p.layer_off;
+  for (int k = blockIdx.y * (kUThreads / 32) + warp; k < min(R, (blockIdx.y + 1) * (kUThreads / 32));
+       k += kUThreads / 32) {
+    const uint4 *a4 = reinterpret_cast<const uint4 *>(slot + (size_t)k * dff);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    int v = lane;
+    for (; v + 96 < nvec; v += 128) {
+      uint4 a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = a4[v + 32 * u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint4 z = xs[v + 32 * u];
+        const __nv_bfloat16 *ah = reinterpret_cast<const __nv_bfloat16 *>(&a[u]);
+        const __nv_bfloat16 *zh = reinterpret_cast<const __nv_bfloat16 *>(&z);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[u] = fmaf(bf(ah[e]), bf(zh[e]), acc[u]);
+      }
+    }
+    for (; v < nvec; v += 32) {
+      const uint4 a = a4[v], z = xs[v];
+      const __nv_bfloat16 *ah = reinterpret_cast<const __nv_bfloat16 *>(&a);
+      const __nv_bfloat16 *zh = reinterpret_cast<const __nv_bfloat16 *>(&z);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[0] = fmaf(bf(ah[e]), bf(zh[e]), acc[0]);
+    }
+    float s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) p.u[(size_t)b * 64 + k] = s;
   }
 }
 
@@ -78,12 +102,31 @@ __global__ void __launch_bounds__(512) lr_write_kernel(const LowRankWrite p) {
   extern __shared__ float sm[];                    // m [d_ff], w [R]
   float *m = sm, *w = sm + p.d_ff;
   const int b = blockIdx.x, o = p.owner_idx[b];
-  const int R = p.rank, dff = p.d_ff, dm = p.d_model, C = p.C;
-  const __nv_bfloat16 *Z = static_cast<const __nv_bfloat16 *>(p.tailZ) + o * p.tz_owner + p.tz_layer;
-  for (int j = threadIdx.x; j < dff; j += blockDim.x) {      // chunk mean m (t ascending)
-    float s = 0.f;
-    for (int t = 0; t < C; ++t) s += bf(Z[(size_t)t * dff + j]);
-    m[j] = s / (float)C;
+  const int R = p.rank, dff = p.d_ff, dm = p.d_model, C = p.C, nvec = dff / 8;
+  const uint4 *Z = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.tailZ) + o * p.tz_owner +
+                                                   p.tz_layer);
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {     // chunk mean m: 8 columns per thread, t ascending
+    float sacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int t = 0;
+    for (; t + 7 < C; t += 8) {                               // 8 independent 16-byte loads in flight
+      uint4 z[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) z[u] = Z[(size_t)(t + u) * nvec + v];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&z[u]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sacc[e] += bf(h[e]);
+      }
+    }
+    for (; t < C; ++t) {
+      const uint4 z = Z[(size_t)t * nvec + v];
+      const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&z);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) sacc[e] += bf(h[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) m[v * 8 + e] = sacc[e] / (float)C;
   }
   __syncthreads();
   const __nv_bfloat16 *src = static_cast<const __nv_bfloat16 *>(p.slots) + (2LL * o + p.sel[o]) * p.slot_elems +
@@ -91,30 +134,52 @@ __global__ void __launch_bounds__(512) lr_write_kernel(const LowRankWrite p) {
   __nv_bfloat16 *dst = static_cast<__nv_bfloat16 *>(p.slots) + (2LL * o + 1 - p.sel[o]) * p.slot_elems + p.layer_off;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int k = warp; k < R; k += nw) {                        // w = A m
+    const uint4 *a4 = reinterpret_cast<const uint4 *>(src + (size_t)k * dff);
     float s = 0.f;
-    for (int j = lane; j < dff; j += 32) s = fmaf(bf(src[(size_t)k * dff + j]), m[j], s);
+    for (int v = lane; v < nvec; v += 32) {
+      const uint4 a = a4[v];
+      const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&a);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s = fmaf(bf(h[e]), m[v * 8 + e], s);
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     if (lane == 0) w[k] = s;
   }
   __syncthreads();
   bool bad = false;
-  for (size_t e = threadIdx.x; e < (size_t)R * dff; e += blockDim.x) {   // A' = A + η w mᵀ
-    const int k = (int)(e / dff), j = (int)(e - (size_t)k * dff);
-    const __nv_bfloat16 a = __float2bfloat16_rn(fmaf(p.eta * w[k], m[j], bf(src[e])));
-    bad |= !isfinite(bf(a));
-    dst[e] = a;
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+  uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+  for (int e = threadIdx.x; e < R * nvec; e += blockDim.x) {   // A' = A + η w mᵀ, 8 elements per thread
+    const int k = e / nvec, v = e - k * nvec;
+    const uint4 a = s4[e];
+    const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&a);
+    uint4 r;
+    __nv_bfloat16 *rh = reinterpret_cast<__nv_bfloat16 *>(&r);
+    const float ew = p.eta * w[k];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      rh[q] = __float2bfloat16_rn(fmaf(ew, m[v * 8 + q], bf(h[q])));
+      bad |= !isfinite(bf(rh[q]));
+    }
+    d4[e] = r;
   }
-  for (size_t e = threadIdx.x; e < (size_t)R * dm; e += blockDim.x)     // B' = B
-    dst[(size_t)R * dff + e] = src[(size_t)R * dff + e];
+  const int nb = R * dm / 8;                                  // B' = B
+  for (int e = threadIdx.x; e < nb; e += blockDim.x) d4[R * nvec + e] = s4[R * nvec + e];
   if (bad) atomicOr(p.fail_flag, 1);
 }
 
 }  // namespace
 
 cudaError_t launch_lowrank_read(const LowRankRead &p, const ChunkLaunch &base, cudaStream_t s) {
-  const int warps = p.n * p.rank;
-  lr_u_kernel<<<(warps * 32 + 255) / 256, 256, 0, s>>>(p);
+  const size_t smem = (size_t)p.d_ff * 2;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e0 = cudaFuncSetAttribute(lr_u_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e0 != cudaSuccess) return e0;
+    configured = smem;
+  }
+  lr_u_kernel<<<dim3(p.n, (p.rank + 31) / 32), kUThreads, smem, s>>>(p);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
