@@ -198,10 +198,19 @@ def main():
 
     assert a.warmup >= 3 or a.max_clock, "W >= 3 warm-up steps"
     profiling = bool(a.max_clock or a.prefill or a.layers != N_LAYERS)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; TTT_SAME_DEVICE=1 + TTT_DIST_BACKEND=gloo run several ranks on one GPU
+    # (multi-rank code-path check on a 1-GPU box; judged runs use NCCL, one GPU per rank)
+    backend = os.environ.get("TTT_DIST_BACKEND", "nccl")
+    local_dev = 0 if os.environ.get("TTT_SAME_DEVICE") == "1" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    from paper_2605_28053_b200 import distributed as D
+    coll_dev = dev if backend == "nccl" else None
     L = a.layers
     window = a.max_clock or CHUNK
     owner_base = 1000 + 100 * rank
@@ -280,10 +289,7 @@ def main():
     ms = e0.elapsed_time(e1)
     read_ms = [x.elapsed_time(y) for x, y in srv.read_events]
     write_ms = [x.elapsed_time(y) for x, y in srv.write_events]
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = D.max_over_ranks(ms, coll_dev)
     tokens_total = world * a.steps * window * N_STREAMS
     value = tokens_total / (ms_max / 1e3)
 
@@ -307,10 +313,8 @@ def main():
             Yh.copy_(src.Y, non_blocking=True)
         f1.record(stream)
         torch.cuda.synchronize(dev)
-        t2 = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        e2e = {"value": tokens_total / (float(t2.item()) / 1e3), "unit": "tok/s",
+        e2e_ms = D.max_over_ranks(f0.elapsed_time(f1), coll_dev)
+        e2e = {"value": tokens_total / (e2e_ms / 1e3), "unit": "tok/s",
                "h2d_bytes_per_step": (Xh.numel() + Vh.numel()) * 2, "d2h_bytes_per_step": Yh.numel() * 2}
 
     if rank == 0:
@@ -330,6 +334,7 @@ def main():
             "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded counter-based RNG in HBM; random-init W_down and dW_0 ~ U(-1,1)/sqrt(d_ff))",
+            "ranks_on_one_device": os.environ.get("TTT_SAME_DEVICE") == "1",
             "config": {"workload": WORKLOAD + ("" if not profiling else
                                                f" [PROFILING ONLY: L={L}, window={window}, prefill={a.prefill}]"),
                        "step": f"one TTT chunk window: {window} decode tokens/stream ({window - 1} READ + 1 WRITE) "
