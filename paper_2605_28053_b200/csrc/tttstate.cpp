@@ -84,7 +84,7 @@ static ttt_status check_shape(const ttt_shape *s) {
     return fail(TTT_E_SHAPE, "backend must be fast-weight (τ=0) or low-rank (τ=1)");
   if (s->backend == TTT_LOW_RANK &&
       (s->rank < 1 || s->rank > 64 || s->dtype != TTT_BF16 || !read_chunk_supported(s->d_model, s->d_ff, 128)))
-    return fail(TTT_E_SHAPE, "low-rank: rank in [1,64], bf16, d_ff % 64 == 0, d_model % 128 (or 160) == 0");
+    return fail(TTT_E_SHAPE, "low-rank: rank in [1,64], bf16, d_ff % 64 == 0, d_model % 16 == 0 (>= 128)");
   if (s->dtype != TTT_BF16 && s->dtype != TTT_FP32) return fail(TTT_E_SHAPE, "dtype");
   if (s->d_model <= 0 || s->d_ff <= 0 || s->chunk <= 0 || s->n_layers <= 0)
     return fail(TTT_E_SHAPE, "non-positive dimension");
@@ -407,7 +407,7 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
     cl.X = lp.Xg; cl.w_down = p->w_down; cl.slots = p->w_down;
     cl.delta = 0; cl.append = 0; cl.Y32 = lp.Y32; cl.valid_rows = g->n;
     // split K so the base GEMM (one or two 128-row blocks) covers the SMs; slabs summed in order
-    const int ntile = cl.n * (sh.d_model % 160 == 0 ? sh.d_model / 160 : sh.d_model / 128);
+    const int ntile = cl.n * ((sh.d_model + 159) / 160);
     cl.ksplit = std::max(1, std::min({kMaxKSplit, device_sm_count() / ntile, sh.d_ff / 64}));
     cl.y32_slab = (long long)align_up((size_t)p->max_owners, 128) * sh.d_model;
     lp.ksplit = cl.ksplit;
@@ -494,7 +494,7 @@ ttt_status read_apply_chunk(ttt_pool *p, const ttt_group *g, int32_t layer, cons
   if (g->effect != TTT_WRITE) return fail(TTT_E_WRONG_EFFECT, "a whole chunk ends in its boundary WRITE");
   if (layer < 0 || layer >= sh.n_layers) return fail(TTT_E_SHAPE, "layer out of range");
   if (sh.backend != TTT_FAST_WEIGHT || sh.dtype != TTT_BF16 || !read_chunk_supported(sh.d_model, sh.d_ff, sh.chunk))
-    return fail(TTT_E_SHAPE, "chunk READ needs bf16, d_ff % 64 == 0, d_model % 128 (or 160) == 0, C <= 128");
+    return fail(TTT_E_SHAPE, "chunk READ needs bf16, d_ff % 64 == 0, d_model % 16 == 0 (>= 128), C <= 128");
   for (int b = 0; b < g->n; ++b) {
     OwnerRec &r = *recs[b];
     if (r.tail_len != 0 || (r.n_applied > 0 && !r.chunk_mode))

@@ -20,7 +20,7 @@ from .gpu_helpers import HostGenInputs, make_engine, read_lowrank  # noqa: E402
 DEV = "cuda"
 
 
-@pytest.mark.parametrize("rank,streams,d_model,d_ff", [(8, 16, 256, 384), (16, 130, 320, 256), (64, 4, 256, 448)])
+@pytest.mark.parametrize("rank,streams,d_model,d_ff", [(8, 16, 256, 384), (16, 130, 320, 256), (64, 4, 256, 448), (16, 6, 400, 256)])
 def test_config4_lowrank_branches_parity(rank, streams, d_model, d_ff):
     tr = T.config4_lowrank(n_steps=26, n_layers=2, rank=rank, d_model=d_model, d_ff=d_ff, chunk=8,
                            n_streams=streams, seed=rank)

@@ -46,8 +46,10 @@ def run_prefill(tr, eng):
 
 
 @pytest.mark.parametrize("d_model,d_ff,chunk,streams", [(320, 384, 16, 3), (256, 448, 64, 2), (384, 256, 128, 2),
-                                                        (640, 512, 48, 9)])
+                                                        (640, 512, 48, 9), (400, 320, 32, 5),
+                                                        (2560, 256, 128, 8)])
 def test_chunk_read_prefill_parity(d_model, d_ff, chunk, streams):
+    # d_model 400 / 2560 exercise the mixed-width N blocks (25 × 16 / 16 × 144 + 2 × 128)
     tr = T.uniform_small(n_streams=streams, n_layers=2, d_model=d_model, d_ff=d_ff, chunk=chunk, n_steps=2 * chunk,
                          dtype="bf16", delta0="rng", v0=4, seed=21)
     eng = make_engine(tr, DEV)
