@@ -33,6 +33,7 @@ struct ReadParams {
   int fuse;                      // f3: also write ΔW + η·v·xᵀ to the shadow slot (C = 1)
   float eta;
   int *fail_flag;
+  int order;                     // task order: 0 CTA-major, 1 SM-interleaved (balanced bytes per SM)
 };
 
 // a5: chunk update of one layer for every member (shadow slot <- ΔW_v + η VᵀZ).

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
   asm volatile("griddepcontrol.launch_dependents;");
   const int n_tasks = (n + 1) * dm;
   const int stride = gridDim.x * kWarps;
-  int t = blockIdx.x * kWarps + warp;
+  int t = p.order ? warp * gridDim.x + blockIdx.x : blockIdx.x * kWarps + warp;
   auto load = [&](uint4 (&buf)[kU], const uint4 *row, int v0) {
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -332,7 +332,10 @@ cudaError_t launch_cfg1(const ReadParams &p, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, read_decode_kernel<T, TH, U, FUSE>, p);
+  static const int order = getenv("TTT_READ_ORDER") ? atoi(getenv("TTT_READ_ORDER")) : 1;
+  ReadParams q = p;
+  q.order = order;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, read_decode_kernel<T, TH, U, FUSE>, q);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }

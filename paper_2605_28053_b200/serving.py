@@ -110,7 +110,7 @@ class Server:
         self.forks: dict = {}
         self.branches: set = set()
         self.clock = 0
-        self.read_events: list = []       # (start, end) CUDA event pairs around read_apply
+        self.read_events: list = []       # (start, end, launches): events around a step's back-to-back READs
         self.write_events: list = []      # (start, end) around write_commit
 
     def admit(self):
@@ -162,14 +162,14 @@ class Server:
             ps = [self.pos[s] for s in ss]
             log.plan.append((g.issue_step, g.effect, ss, [self.ready_at[s] for s in ss]))
             prof = self.profile and clock % self.profile_every == 0
+            if prof:                    # one event pair per group: per-launch events would break PDL overlap
+                e0 = self._ev()
             for l in range(tr.n_layers):                                # ExecuteOperatorGroup
                 X, xr, Vt, vr, Y, yr = src.group_io(l, ss, ps)
-                if prof:
-                    e0 = self._ev()
                 capi.read_apply(pool, g, l, X, xr, Vt, vr, Y, yr, None, stream)
-                if prof:
-                    self.read_events.append((e0, self._ev()))
                 src.on_output(l, ss, ps, Y, yr)                         # ReturnOutputs
+            if prof:
+                self.read_events.append((e0, self._ev(), tr.n_layers))
             log.census[g.effect] += len(ss)
             if g.effect == READ:
                 capi.tttstate_step_done(pool, g)                        # UpdateKVAndTailMetadata
