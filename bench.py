@@ -277,6 +277,8 @@ def main():
     barrier()
     torch.cuda.synchronize(dev)
     n_launch0 = capi.tttstate_launch_count()
+    plan0, census0 = srv.plan_s, dict(srv.log.census)
+    wall0 = time.perf_counter()
     with ClockSampler(local) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -285,6 +287,9 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize(dev)
     n_launch = capi.tttstate_launch_count() - n_launch0
+    wall_s = time.perf_counter() - wall0
+    plan_s = srv.plan_s - plan0
+    census = {("READ" if k == 0 else "WRITE"): v - census0.get(k, 0) for k, v in srv.log.census.items()}
     barrier()
     ms = e0.elapsed_time(e1)
     read_spans = [(x.elapsed_time(y), n) for x, y, n in srv.read_events]
@@ -355,6 +360,9 @@ def main():
             traffic = json.load(open(tf)).get("read_decode_kernel", {}).get("dram_bytes_per_launch")
         write_bytes = N_STREAMS * (2 * D_MODEL * D_FF * 2 + CHUNK * (D_FF + D_MODEL) * 2) * L
         write_avg = sum(write_ms) / len(write_ms) if write_ms else None
+        # whole-step roofline: every byte of the window's READs and its boundary WRITE at HBM peak
+        roof_ms = (window * L * read_bytes + write_bytes) / (hbm * 1e9) * 1e3
+        roof_tok_s = window * N_STREAMS / (roof_ms / 1e3)
         out = {
             "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
@@ -382,6 +390,12 @@ def main():
                       "alg_bytes_per_call": write_bytes},
             # READ launches per timed window: L per decode step; events sample 1 step in 8
             "read_share_of_step": read_avg * L * window * a.steps / ms,
+            "step_roofline": {"ms_per_step": roof_ms, "tok_s_per_gpu": roof_tok_s,
+                              "frac": (value / world) / roof_tok_s,
+                              "bytes_per_step": window * L * read_bytes + write_bytes},
+            "census": census,
+            "planner_host_share": plan_s / wall_s,
+            "host_wall_ms_per_step": wall_s * 1e3 / a.steps,
             "clocks": clk.summary(),
         }
         if world == 1 and not a.no_cpu_baseline:

@@ -8,6 +8,7 @@
 
 namespace ttt {
 
+constexpr int kMaxLrSeg = 16;          // low-rank READ: max K segments per A row
 constexpr int kMaxReadMembers = 8;     // members per READ launch (X rows staged in smem)
 constexpr int kMaxGroup = 256;         // members per group (planner B cap)
 constexpr int kMaxKSplit = 16;         // low-rank base GEMM split-K slabs
@@ -75,6 +76,9 @@ struct ChunkLaunch {
   int ksplit = 1;                // base mode: K split in `ksplit` ranges, slab ks at Y32 + ks*y32_slab
   long long y32_slab = 0;
   int owner_idx[kMaxGroup];
+  const struct LowRankRead *lr = nullptr;   // non-null: fused low-rank READ (u = A x, finish) in this launch
+  int *lr_ctr = nullptr;                    // fused mode counters [u_done, exit, tickets...], zero at rest
+  int x_rowmap = 0;                         // X is [rows][d_ff] (2-D map, rows past n zero-filled)
 };
 
 // NEXT f1: low-rank delta READ / WRITE (DeltaAdapterState).
@@ -82,8 +86,10 @@ struct LowRankRead {
   int n, d_model, d_ff, rank;
   const void *X, *Vt, *resid;
   void *Y, *Xg;
-  float *Y32, *u;                // [ksplit][rows][d_model] base product slabs, [n][64] A·x
+  float *Y32, *u;                // [ksplit][rows][d_model] base product slabs, [n·R][nseg] A·x partials
   int ksplit;
+  int nseg;                      // A rows split into nseg K segments (one warp task each)
+  int *ctr;                      // fused-mode counters (see ChunkLaunch::lr_ctr)
   long long y32_slab;
   const void *slots;
   long long slot_elems, layer_off;
@@ -103,6 +109,7 @@ struct LowRankWrite {
   int *fail_flag;
   int owner_idx[kMaxGroup];
 };
+bool read_chunk_fused_fits(int row_blocks, int d_model, int ksplit);
 cudaError_t launch_lowrank_read(const LowRankRead &p, const ChunkLaunch &base, cudaStream_t s);
 cudaError_t launch_lowrank_write(const LowRankWrite &p, cudaStream_t s);
 

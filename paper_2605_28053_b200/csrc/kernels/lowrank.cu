@@ -15,6 +15,8 @@
 // B copied; a non-finite candidate raises the group fail flag.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "../internal.h"
 
 namespace ttt {
@@ -22,79 +24,136 @@ namespace {
 
 __device__ __forceinline__ float bf(const __nv_bfloat16 v) { return __bfloat162float(v); }
 
-// one CTA per member b: x_b staged in shared memory once, warps over the rank rows k,
-// 4 independent 16-byte loads of A in flight per lane.
-constexpr int kUThreads = 1024;                   // 32 warps = 32 rank rows per CTA
-__global__ void __launch_bounds__(kUThreads) lr_u_kernel(const LowRankRead p) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint4 *xs = reinterpret_cast<uint4 *>(smem);
-  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int R = p.rank, dff = p.d_ff, dm = p.d_model, nvec = dff / 8;
-  const bool first = blockIdx.y == 0;              // rank block 0 also gathers x and appends the tail
-  const int o = p.owner_idx[b];
-  const uint4 *x4 = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff);
-  uint4 *xg = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.Xg) + (size_t)b * dff);
-  uint4 *tz = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.tailZ) + o * p.tz_owner + p.tz_layer +
-                                        (size_t)p.tail_pos[b] * dff);
-  for (int v = tid; v < nvec; v += kUThreads) {     // stage x; gather for the base GEMM; tail append (a4)
-    const uint4 z = x4[v];
-    xs[v] = z;
-    if (first) {
-      xg[v] = z;
-      tz[v] = z;
-    }
+typedef unsigned long long u64;
+__device__ __forceinline__ uint4 ld_stream(const uint4 *q) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(q));
+  return r;
+}
+// acc += a.lo*z.lo + a.hi*z.hi for one packed bf16 pair, fp32 accumulate (FHFMA.BF16)
+__device__ __forceinline__ void fma_bf16x2(float &acc, uint32_t a, uint32_t z) {
+  asm("{\n\t.reg .b16 al, ah, zl, zh;\n\t"
+      "mov.b32 {al, ah}, %1;\n\tmov.b32 {zl, zh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, al, zl, %0;\n\tfma.rn.f32.bf16 %0, ah, zh, %0;\n}"
+      : "+f"(acc)
+      : "r"(a), "r"(z));
+}
+__device__ __forceinline__ void dot8(float &acc, const uint4 &a, const uint4 &z) {
+  fma_bf16x2(acc, a.x, z.x); fma_bf16x2(acc, a.y, z.y); fma_bf16x2(acc, a.z, z.z); fma_bf16x2(acc, a.w, z.w);
+}
+
+// u = A x as warp tasks (member b, rank row k, K segment j of nseg): a persistent grid of
+// 1024-thread CTAs on every SM streams A with 4 × 16-byte loads per lane in flight (x from
+// L2), each task writes its partial to u[(b·R + k)·nseg + j] and lr_finish sums the nseg
+// partials in order (deterministic).  The same launch gathers x into the contiguous
+// workspace of the base GEMM (when rows are not already contiguous) and appends the tail.
+constexpr int kUThreads = 1024;
+__global__ void __launch_bounds__(kUThreads, 1) lr_u_kernel(const LowRankRead p, int gather) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int R = p.rank, dff = p.d_ff, dm = p.d_model, nvec = dff / 8, S = p.nseg;
+  const int gtid = blockIdx.x * kUThreads + tid, gsz = gridDim.x * kUThreads;
+  for (int idx = gtid; idx < p.n * nvec; idx += gsz) {       // gather x, append z (a4)
+    const int b = idx / nvec, v = idx - b * nvec, o = p.owner_idx[b];
+    const uint4 z = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff)[v];
+    if (gather) reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.Xg) + (size_t)b * dff)[v] = z;
+    reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.tailZ) + o * p.tz_owner + p.tz_layer +
+                              (size_t)p.tail_pos[b] * dff)[v] = z;
   }
-  if (first) {
-    const __nv_bfloat16 *vt = static_cast<const __nv_bfloat16 *>(p.Vt) + (size_t)p.v_row[b] * dm;
-    __nv_bfloat16 *tv = static_cast<__nv_bfloat16 *>(p.tailV) + o * p.tv_owner + p.tv_layer + (size_t)p.tail_pos[b] * dm;
-    for (int i = tid; i < dm; i += kUThreads) tv[i] = vt[i];
+  for (int idx = gtid; idx < p.n * dm; idx += gsz) {         // append v
+    const int b = idx / dm, i = idx - b * dm, o = p.owner_idx[b];
+    (static_cast<__nv_bfloat16 *>(p.tailV) + o * p.tv_owner + p.tv_layer + (size_t)p.tail_pos[b] * dm)[i] =
+        (static_cast<const __nv_bfloat16 *>(p.Vt) + (size_t)p.v_row[b] * dm)[i];
   }
-  __syncthreads();
-  const __nv_bfloat16 *slot = static_cast<const __nv_bfloat16 *>(p.slots) +
-                              (2LL * o + p.sel[o]) * p.slot_elems + p.layer_off;
-  for (int k = blockIdx.y * (kUThreads / 32) + warp; k < min(R, (blockIdx.y + 1) * (kUThreads / 32));
-       k += kUThreads / 32) {
-    const uint4 *a4 = reinterpret_cast<const uint4 *>(slot + (size_t)k * dff);
+  const int n_tasks = p.n * R * S, nw = gridDim.x * (kUThreads / 32);
+  for (int t = warp * gridDim.x + blockIdx.x; t < n_tasks; t += nw) {
+    const int r = t / S, j = t - r * S, b = r / R, k = r - b * R, o = p.owner_idx[b];
+    const uint4 *a4 = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.slots) +
+                                                      (2LL * o + p.sel[o]) * p.slot_elems + p.layer_off +
+                                                      (size_t)k * dff);
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff);
+    const int v0 = nvec * j / S, v1 = nvec * (j + 1) / S;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    int v = lane;
-    for (; v + 96 < nvec; v += 128) {
-      uint4 a[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = a4[v + 32 * u];
+    for (int v = v0 + lane; v < v1; v += 128) {
+      uint4 a[4], z[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint4 z = xs[v + 32 * u];
-        const __nv_bfloat16 *ah = reinterpret_cast<const __nv_bfloat16 *>(&a[u]);
-        const __nv_bfloat16 *zh = reinterpret_cast<const __nv_bfloat16 *>(&z);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[u] = fmaf(bf(ah[e]), bf(zh[e]), acc[u]);
+        const bool in = v + 32 * u < v1;
+        a[u] = in ? ld_stream(a4 + v + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
+        z[u] = in ? __ldg(x4 + v + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
       }
-    }
-    for (; v < nvec; v += 32) {
-      const uint4 a = a4[v], z = xs[v];
-      const __nv_bfloat16 *ah = reinterpret_cast<const __nv_bfloat16 *>(&a);
-      const __nv_bfloat16 *zh = reinterpret_cast<const __nv_bfloat16 *>(&z);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[0] = fmaf(bf(ah[e]), bf(zh[e]), acc[0]);
+      for (int u = 0; u < 4; ++u) dot8(acc[u], a[u], z[u]);
     }
     float s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) p.u[(size_t)b * 64 + k] = s;
+    if (lane == 0) p.u[(size_t)r * S + j] = s;
   }
 }
 
-__global__ void __launch_bounds__(256) lr_finish_kernel(const LowRankRead p) {
-  const int b = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= p.n || i >= p.d_model) return;
-  const int o = p.owner_idx[b];
+// y_b = Σ_ks Y32[ks]_b + Bᵀ u_b (+ residual): one CTA per (member, 2048 outputs), 8 outputs
+// per thread with 16-byte loads; u_b = Σ_j partials (in order) staged in shared memory.
+constexpr int kFinThreads = 256;
+__global__ void __launch_bounds__(kFinThreads) lr_finish_kernel(const LowRankRead p) {
+  __shared__ float us[64];
+  const int b = blockIdx.y, o = p.owner_idx[b], R = p.rank, dm = p.d_model, S = p.nseg;
+  if (threadIdx.x < R) {
+    float u = 0.f;
+    for (int j = 0; j < S; ++j) u += p.u[((size_t)b * R + threadIdx.x) * S + j];
+    us[threadIdx.x] = u;
+  }
+  __syncthreads();
+  const int i0 = (blockIdx.x * kFinThreads + threadIdx.x) * 8;
+  if (i0 >= dm) return;
   const __nv_bfloat16 *Bm = static_cast<const __nv_bfloat16 *>(p.slots) + (2LL * o + p.sel[o]) * p.slot_elems +
-                            p.layer_off + (size_t)p.rank * p.d_ff;
-  float y = 0.f;
-  for (int ks = 0; ks < p.ksplit; ++ks) y += p.Y32[ks * p.y32_slab + (size_t)b * p.d_model + i];   // fixed order
-  for (int k = 0; k < p.rank; ++k) y = fmaf(p.u[(size_t)b * 64 + k], bf(Bm[(size_t)k * p.d_model + i]), y);
-  if (p.resid) y += bf(static_cast<const __nv_bfloat16 *>(p.resid)[(size_t)p.y_row[b] * p.d_model + i]);
-  static_cast<__nv_bfloat16 *>(p.Y)[(size_t)p.y_row[b] * p.d_model + i] = __float2bfloat16_rn(y);
+                            p.layer_off + (size_t)R * p.d_ff;
+  float y[8];
+  {
+    const float4 *q = reinterpret_cast<const float4 *>(p.Y32 + (size_t)b * dm + i0);
+    const float4 lo = q[0], hi = q[1];
+    y[0] = lo.x; y[1] = lo.y; y[2] = lo.z; y[3] = lo.w; y[4] = hi.x; y[5] = hi.y; y[6] = hi.z; y[7] = hi.w;
+  }
+  for (int ks = 1; ks < p.ksplit; ++ks) {                     // fixed slab order
+    const float4 *q = reinterpret_cast<const float4 *>(p.Y32 + ks * p.y32_slab + (size_t)b * dm + i0);
+    const float4 lo = q[0], hi = q[1];
+    y[0] += lo.x; y[1] += lo.y; y[2] += lo.z; y[3] += lo.w; y[4] += hi.x; y[5] += hi.y; y[6] += hi.z; y[7] += hi.w;
+  }
+  for (int k0 = 0; k0 < R; k0 += 8) {              // 8 B rows' loads in flight
+    uint4 bv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      bv[q] = k0 + q < R ? *reinterpret_cast<const uint4 *>(Bm + (size_t)(k0 + q) * dm + i0) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t w[4] = {bv[q].x, bv[q].y, bv[q].z, bv[q].w};
+      const float uk = k0 + q < R ? us[k0 + q] : 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        y[2 * e] = fmaf(uk, __uint_as_float(w[e] << 16), y[2 * e]);
+        y[2 * e + 1] = fmaf(uk, __uint_as_float(w[e] & 0xffff0000u), y[2 * e + 1]);
+      }
+    }
+  }
+  if (p.resid) {
+    const uint4 rv = *reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.resid) +
+                                                      (size_t)p.y_row[b] * dm + i0);
+    const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      y[2 * e] += __uint_as_float(w[e] << 16);
+      y[2 * e + 1] += __uint_as_float(w[e] & 0xffff0000u);
+    }
+  }
+  uint32_t out[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(y[2 * e], y[2 * e + 1]);
+    out[e] = *reinterpret_cast<uint32_t *>(&h);
+  }
+  *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.Y) + (size_t)p.y_row[b] * dm + i0) =
+      make_uint4(out[0], out[1], out[2], out[3]);
 }
 
 // one CTA per member (grid.x = n), one layer per launch
@@ -169,23 +228,66 @@ __global__ void __launch_bounds__(512) lr_write_kernel(const LowRankWrite p) {
   if (bad) atomicOr(p.fail_flag, 1);
 }
 
+__global__ void __launch_bounds__(256) lr_gather_kernel(const LowRankRead p) {
+  const int nvec = p.d_ff / 8;
+  for (int idx = blockIdx.x * 256 + threadIdx.x; idx < p.n * nvec; idx += gridDim.x * 256) {
+    const int b = idx / nvec, v = idx - b * nvec;
+    reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.Xg) + (size_t)b * p.d_ff)[v] =
+        reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * p.d_ff)[v];
+  }
+}
+
 }  // namespace
 
-cudaError_t launch_lowrank_read(const LowRankRead &p, const ChunkLaunch &base, cudaStream_t s) {
-  const size_t smem = (size_t)p.d_ff * 2;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e0 = cudaFuncSetAttribute(lr_u_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e0 != cudaSuccess) return e0;
-    configured = smem;
+// K segments per A row so the n·R·nseg warp tasks fill whole waves of warps
+int lr_segments(int rows, int warps) {
+  int best = 1;
+  double best_eff = 0;
+  for (int S = 1; S <= kMaxLrSeg; ++S) {
+    const long long t = (long long)rows * S;
+    const double eff = (double)t / ((double)((t + warps - 1) / warps) * warps);
+    if (eff > best_eff + 1e-3) {
+      best_eff = eff;
+      best = S;
+    }
   }
-  lr_u_kernel<<<dim3(p.n, (p.rank + 31) / 32), kUThreads, smem, s>>>(p);
+  return best;
+}
+
+cudaError_t launch_lowrank_read(const LowRankRead &p0, const ChunkLaunch &base0, cudaStream_t s) {
+  LowRankRead p = p0;
+  ChunkLaunch base = base0;
+  const int sms = device_sm_count();
+  static const bool fused_on = !getenv("TTT_LR_FUSED") || atoi(getenv("TTT_LR_FUSED")) != 0;
+  if (fused_on && read_chunk_fused_fits(base.n, p.d_model, base.ksplit)) {
+    // one launch: base GEMM on tcgen05 + u = A x warps + tail append + finish (read_chunk_tc.cu)
+    bool identity = true;
+    for (int b = 0; b < p.n; ++b) identity &= p.x_row[b] == b;
+    if (identity) {
+      base.X = p.X;
+      base.x_rowmap = 1;
+    } else {
+      lr_gather_kernel<<<sms * 4, 256, 0, s>>>(p);
+      count_launch();
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    base.lr = &p;
+    base.lr_ctr = p.ctr;
+    return launch_read_chunk(base, s);
+  }
+  p.nseg = lr_segments(p.n * p.rank, sms * (kUThreads / 32));
+  // the base GEMM reads X in place when its rows are 0..n-1 and fill whole 128-row blocks
+  int gather = p.n % 128 != 0;
+  for (int b = 0; b < p.n; ++b) gather |= p.x_row[b] != b;
+  if (!gather) base.X = p.X;
+  lr_u_kernel<<<sms, kUThreads, 0, s>>>(p, gather);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   e = launch_read_chunk(base, s);                  // base-only tcgen05 GEMM into Y32
   if (e != cudaSuccess) return e;
-  lr_finish_kernel<<<dim3((p.d_model + 255) / 256, p.n), 256, 0, s>>>(p);
+  lr_finish_kernel<<<dim3((p.d_model / 8 + kFinThreads - 1) / kFinThreads, p.n), kFinThreads, 0, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }

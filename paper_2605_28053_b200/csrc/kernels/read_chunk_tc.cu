@@ -20,6 +20,8 @@
 //    swizzle), warp 1 TMEM alloc + single-thread MMA issue, warps 2-5
 //    epilogue (tcgen05.ld → bf16 → Y); during the mainloop the epilogue warps
 //    of each of a member's N-tiles append 1/nt of the chunk to the tail.
+#include <mutex>
+
 #include "../internal.h"
 #include "sm100_ptx.cuh"
 
@@ -30,6 +32,22 @@ using namespace ptx;
 
 constexpr int BM = 128, BK = 64, kStages = 4;
 constexpr int kThreads = 192;
+constexpr int kUW = 16;                           // fused low-rank mode: u = A x warps per CTA
+constexpr int kThreadsLR = kThreads + 32 * kUW;
+
+// fused low-rank READ (NEXT f1) extras: the u = A x stream, the tail append and the finish
+// y = Σ_ks Y32 + Bᵀu (+ resid) run inside the base-GEMM launch (one launch per layer)
+struct LrFused {
+  const void *slots;
+  long long slot_elems, layer_off;
+  int R;
+  const void *Xsrc, *resid;
+  void *Yout;
+  float *u;                      // [n][R]
+  float *bu;                     // [n][d_model] Bᵀu per member (fp32)
+  int *ctr;                      // [0] members whose Bᵀu is done, [1] CTAs exited, [2..] slab tickets per (row block, N block)
+  int x_row[kMaxGroup], v_row[kMaxGroup], y_row[kMaxGroup], tail_pos[kMaxGroup];
+};
 
 struct ChunkParams {
   int n, d_model, d_ff, C, L, layer;
@@ -42,22 +60,105 @@ struct ChunkParams {
   int nt, w_hi, h;               // N blocks per member; blocks j < h are w_hi wide, the rest w_hi - 16
   float *Y32;
   long long y32_slab;
+  int x_rowmap;                  // X map is [rows][d_ff]: row block b starts at row 128·b
   int owner_idx[kMaxGroup];
+  LrFused lr;
 };
 
-template <int BN>   // BN: largest N-block (smem stage size); actual widths are runtime
-__global__ void __launch_bounds__(kThreads, 1)
+__device__ __forceinline__ uint4 ld_stream(const uint4 *q) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(q));
+  return r;
+}
+__device__ __forceinline__ void fma_bf16x2(float &acc, uint32_t a, uint32_t z) {
+  asm("{\n\t.reg .b16 al, ah, zl, zh;\n\t"
+      "mov.b32 {al, ah}, %1;\n\tmov.b32 {zl, zh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, al, zl, %0;\n\tfma.rn.f32.bf16 %0, ah, zh, %0;\n}"
+      : "+f"(acc)
+      : "r"(a), "r"(z));
+}
+__device__ __forceinline__ int ld_volatile(const int *q) {
+  int v;
+  asm volatile("ld.volatile.global.b32 %0, [%1];" : "=r"(v) : "l"(q));
+  return v;
+}
+
+// f1 finish, run by the 4 epilogue warps + the kUW u warps of the CTA after named barrier 2:
+// y = Σ_ks Y32[ks] + Bᵀu (+ resid) for this tile's columns and its 1/KS share of the rows,
+// 8 outputs per item with the R loads of u and B issued 8 at a time.
+template <int BN>
+__device__ __forceinline__ void lr_finish(const ChunkParams &p, int b, int j, int ks, int n0, int width, int ft) {
+  asm volatile("bar.sync 2, %0;" ::"n"(128 + 32 * kUW) : "memory");
+  const LrFused &lr = p.lr;
+  const int KS = p.ksplit;
+  const int rows = min(BM, p.valid_rows - b * BM), r_lo = rows * ks / KS, r_hi = rows * (ks + 1) / KS;
+  const int cpr = width / 8, items = (r_hi - r_lo) * cpr, dm = p.d_model;
+  for (int itm = ft; itm < items; itm += 128 + 32 * kUW) {
+    const int rr = b * BM + r_lo + itm / cpr, c = n0 + 8 * (itm % cpr);
+    float y[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) y[e] = 0.f;
+    for (int q0 = 0; q0 < KS; q0 += 4) {           // fixed slab order, 4 slabs' loads in flight
+      float4 lo[4], hi[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (q0 + q < KS) {
+          const float4 *s4 = reinterpret_cast<const float4 *>(p.Y32 + (q0 + q) * p.y32_slab + (size_t)rr * dm + c);
+          lo[q] = __ldcg(s4);
+          hi[q] = __ldcg(s4 + 1);
+        } else {
+          lo[q] = hi[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        y[0] += lo[q].x; y[1] += lo[q].y; y[2] += lo[q].z; y[3] += lo[q].w;
+        y[4] += hi[q].x; y[5] += hi[q].y; y[6] += hi[q].z; y[7] += hi[q].w;
+      }
+    }
+    {                                              // + Bᵀu (computed by the member's u warps)
+      const float4 *b4 = reinterpret_cast<const float4 *>(lr.bu + (size_t)rr * dm + c);
+      const float4 lo = __ldcg(b4), hi = __ldcg(b4 + 1);
+      y[0] += lo.x; y[1] += lo.y; y[2] += lo.z; y[3] += lo.w; y[4] += hi.x; y[5] += hi.y; y[6] += hi.z; y[7] += hi.w;
+    }
+    if (lr.resid) {
+      const uint4 rv = *reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(lr.resid) +
+                                                        (size_t)lr.y_row[rr] * dm + c);
+      const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        y[2 * h] += __uint_as_float(w[h] << 16);
+        y[2 * h + 1] += __uint_as_float(w[h] & 0xffff0000u);
+      }
+    }
+    uint32_t out[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(y[2 * h], y[2 * h + 1]);
+      out[h] = *reinterpret_cast<uint32_t *>(&h2);
+    }
+    *reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(lr.Yout) + (size_t)lr.y_row[rr] * dm + c) =
+        make_uint4(out[0], out[1], out[2], out[3]);
+  }
+}
+
+template <int BN, bool LR>   // BN: largest N-block (smem stage size); actual widths are runtime
+__global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
     read_chunk_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                          const __grid_constant__ CUtensorMap tmD, const ChunkParams p) {
   constexpr int kTmemCols = BN <= 128 ? 128 : 256;
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;   // stage slots sized for BN rows
   const uint32_t b_box = (uint32_t)p.w_hi * BK * 2;                   // bytes one B box actually lands
-  constexpr uint32_t STAGE = A_BYTES + 2 * B_BYTES;
+  constexpr uint32_t STAGE = A_BYTES + (LR ? 1 : 2) * B_BYTES;      // low-rank base mode has no ΔW box
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   u64 *bars = reinterpret_cast<u64 *>(smem + kStages * STAGE);
   u64 *full = bars, *empty = bars + kStages, *t_full = bars + 2 * kStages, *t_empty = t_full + 1;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(t_empty + 1);
+  uint4 *xs_lr = reinterpret_cast<uint4 *>(smem + kStages * STAGE + 512);   // LR: one member's x row
+  float *us_lr = reinterpret_cast<float *>(smem + kStages * STAGE + 256);   // LR: u_m = A_m x_m (≤ 64)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = p.nt, nk_all = p.d_ff / BK, KS = p.ksplit;
@@ -104,7 +205,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (it >= kStages) mbar_wait(empty + s, ((it / kStages) - 1) & 1);
           unsigned char *st = smem + s * STAGE;
           mbar_expect_tx(full + s, A_BYTES + (p.delta ? 2 : 1) * b_box);
-          tma_load_3d(st, &tmX, full + s, kb * BK, 0, b);
+          if (p.x_rowmap) tma_load_3d(st, &tmX, full + s, kb * BK, b * BM, 0);
+          else tma_load_3d(st, &tmX, full + s, kb * BK, 0, b);
           tma_load_3d(st + A_BYTES, &tmW, full + s, kb * BK, n0_of(j), p.layer);
           if (p.delta) tma_load_3d(st + A_BYTES + B_BYTES, &tmD, full + s, kb * BK, n0_of(j), slot_l);
         }
@@ -137,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
-  } else {                                                  // ---------------- epilogue warps 2-5
+  } else if (warp < 6) {                                    // ---------------- epilogue warps 2-5
     const int q = warp & 3, row = q * 32 + lane;            // token index t in the chunk
     const int et = threadIdx.x - 64;
     int k = 0;
@@ -194,31 +296,137 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(t_empty);
+      if (LR) {                                    // f1: arm the finish of this tile
+        asm volatile("bar.sync 1, 128;" ::: "memory");   // this CTA's slab is written
+        if (et == 0) {
+          int *tick = p.lr.ctr + 2 + b * nt + j;
+          __threadfence();
+          atomicAdd(tick, 1);
+          while (ld_volatile(tick) < KS) __nanosleep(64);            // every K slab of the tile
+          while (ld_volatile(p.lr.ctr) < p.valid_rows) __nanosleep(64);   // every member's Bᵀu
+          __threadfence();
+        }
+        lr_finish<BN>(p, b, j, ks, n0, width, et);   // with the u warps (named barrier 2)
+      }
     }
+  } else if (LR) {                                          // ---------------- u = A x warps (f1)
+    // CTA c owns members c, c + grid, ...: x_m staged in shared memory once, the kUW warps
+    // stream the R rows of A_m (8 × 16-byte loads per lane in flight), then append (z, v).
+    const LrFused &lr = p.lr;
+    const int uw = warp - 6, ut = uw * 32 + lane, R = lr.R, dff = p.d_ff, dm = p.d_model, nvec = dff / 8;
+    for (int m = blockIdx.x; m < p.valid_rows; m += gridDim.x) {
+      const int o = p.owner_idx[m];
+      const uint4 *x4 = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(lr.Xsrc) +
+                                                        (size_t)lr.x_row[m] * dff);
+      uint4 *tz = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.tailZ) + o * p.tz_owner + p.tz_layer +
+                                            (size_t)lr.tail_pos[m] * dff);
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * kUW) : "memory");   // previous member's rows done
+      for (int v = ut; v < nvec; v += 32 * kUW) {    // stage x_m; a4: append z_m
+        const uint4 z = x4[v];
+        xs_lr[v] = z;
+        tz[v] = z;
+      }
+      {                                              // a4: append v_m
+        const uint4 *vs = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.Vt) +
+                                                          (size_t)lr.v_row[m] * dm);
+        uint4 *tv = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.tailV) + o * p.tv_owner + p.tv_layer +
+                                              (size_t)lr.tail_pos[m] * dm);
+        for (int v = ut; v < dm / 8; v += 32 * kUW) tv[v] = vs[v];
+      }
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * kUW) : "memory");   // x_m staged
+      const __nv_bfloat16 *A = static_cast<const __nv_bfloat16 *>(lr.slots) + (2LL * o + p.sel[o]) * lr.slot_elems +
+                               lr.layer_off;
+      for (int k = uw; k < R; k += kUW) {
+        const uint4 *a4 = reinterpret_cast<const uint4 *>(A + (size_t)k * dff);
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int v = lane; v < nvec; v += 256) {
+          uint4 a[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) a[q] = v + 32 * q < nvec ? ld_stream(a4 + v + 32 * q) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (v + 32 * q < nvec) {
+              const uint4 z = xs_lr[v + 32 * q];
+              float &ac = acc[q & 3];
+              fma_bf16x2(ac, a[q].x, z.x); fma_bf16x2(ac, a[q].y, z.y);
+              fma_bf16x2(ac, a[q].z, z.z); fma_bf16x2(ac, a[q].w, z.w);
+            }
+          }
+        }
+        float sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        if (lane == 0) us_lr[k] = sum;
+      }
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * kUW) : "memory");   // u_m complete (shared memory)
+      // Bᵀu_m: 8 outputs per thread, the R rows of B_m streamed 8 loads at a time
+      const uint4 *B4 = reinterpret_cast<const uint4 *>(A + (size_t)R * dff);
+      for (int i8 = ut; i8 < dm / 8; i8 += 32 * kUW) {
+        float y[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) y[e] = 0.f;
+        for (int k0 = 0; k0 < R; k0 += 8) {
+          uint4 bv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            bv[q] = k0 + q < R ? ld_stream(B4 + (size_t)(k0 + q) * (dm / 8) + i8) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float uk = k0 + q < R ? us_lr[k0 + q] : 0.f;
+            const uint32_t w[4] = {bv[q].x, bv[q].y, bv[q].z, bv[q].w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              y[2 * h] = fmaf(uk, __uint_as_float(w[h] << 16), y[2 * h]);
+              y[2 * h + 1] = fmaf(uk, __uint_as_float(w[h] & 0xffff0000u), y[2 * h + 1]);
+            }
+          }
+        }
+        float4 *o4 = reinterpret_cast<float4 *>(lr.bu + (size_t)m * dm + 8 * i8);
+        o4[0] = make_float4(y[0], y[1], y[2], y[3]);
+        o4[1] = make_float4(y[4], y[5], y[6], y[7]);
+      }
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * kUW) : "memory");   // Bᵀu_m written
+      if (ut == 0) {
+        __threadfence();
+        atomicAdd(lr.ctr, 1);
+      }
+    }
+    int b, j, kb0, kb1;                            // this CTA's (single) tile
+    decode(blockIdx.x, b, j, kb0, kb1);
+    lr_finish<BN>(p, b, j, blockIdx.x % KS, n0_of(j), width_of(j), 128 + uw * 32 + lane);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
+  if (LR && threadIdx.x == 0) {                    // the last CTA out re-arms the counters
+    __threadfence();
+    if (atomicAdd(p.lr.ctr + 1, 1) == (int)gridDim.x - 1) {
+      p.lr.ctr[0] = 0;
+      for (int g = 0; g < p.n * nt; ++g) p.lr.ctr[2 + g] = 0;
+      __threadfence();
+      p.lr.ctr[1] = 0;
+    }
+  }
 }
 
-template <int BN>
-size_t smem_bytes() {
-  return 1024 + (size_t)kStages * (BM * BK * 2 + 2 * BN * BK * 2) + 256;
+template <int BN, bool LR>
+size_t smem_bytes(int d_ff) {   // LR: stages without the ΔW box, plus one x row
+  return 1024 + (size_t)kStages * (BM * BK * 2 + (LR ? 1 : 2) * BN * BK * 2) + 256 + (LR ? 256 + (size_t)d_ff * 2 : 0);
 }
 
-template <int BN>
+template <int BN, bool LR>
 cudaError_t launch_bn(const CUtensorMap &mX, const CUtensorMap &mW, const CUtensorMap &mD, const ChunkParams &p,
                       cudaStream_t s) {
-  const size_t smem = smem_bytes<BN>();
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(read_chunk_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = smem_bytes<BN, LR>(p.d_ff);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(read_chunk_tc_kernel<BN, LR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured = smem;
   }
   const int tiles = p.n * p.nt * p.ksplit;
-  read_chunk_tc_kernel<BN><<<std::min(device_sm_count(), tiles), kThreads, smem, s>>>(mX, mW, mD, p);
+  read_chunk_tc_kernel<BN, LR><<<std::min(device_sm_count(), tiles), LR ? kThreadsLR : kThreads, smem, s>>>(mX, mW, mD, p);
   count_launch();
   return cudaGetLastError();
 }
@@ -251,6 +459,41 @@ NPlan plan_n(int d_model, int tiles_per_block_unit, int sms) {
 
 }  // namespace
 
+// Tensor-map encode cache (host): decode-time launches reuse the same handful of maps per
+// layer, so encoding is done once per (base, dims, box).
+bool cached_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1) {
+  struct Entry {
+    const void *base;
+    uint64_t d0, d1, d2;
+    uint32_t b0, b1;
+    CUtensorMap map;
+  };
+  static Entry cache[128];
+  static int n_used = 0, next = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < n_used; ++i) {
+    const Entry &e = cache[i];
+    if (e.base == base && e.d0 == d0 && e.d1 == d1 && e.d2 == d2 && e.b0 == b0 && e.b1 == b1) {
+      *m = e.map;
+      return true;
+    }
+  }
+  if (!ptx::make_map_bf16_3d(m, base, d0, d1, d2, b0, b1)) return false;
+  Entry &e = cache[next];
+  e = Entry{base, d0, d1, d2, b0, b1, *m};
+  next = (next + 1) % 128;
+  n_used = n_used < 128 ? n_used + 1 : 128;
+  return true;
+}
+
+// fused low-rank READ needs every tile of the launch resident at once (one CTA per SM)
+bool read_chunk_fused_fits(int row_blocks, int d_model, int ksplit) {
+  const int sms = device_sm_count();
+  const NPlan np = plan_n(d_model, row_blocks * std::max(1, ksplit), sms);
+  return np.T > 0 && row_blocks * np.T * std::max(1, ksplit) <= sms;
+}
+
 bool read_chunk_supported(int d_model, int d_ff, int C) {
   return C >= 1 && C <= BM && d_ff % BK == 0 && d_model % 16 == 0 && d_model >= 128 &&
          ptx::encode_fn() != nullptr;
@@ -280,6 +523,7 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
   p.Y32 = cl.Y32;
   p.ksplit = cl.ksplit < 1 ? 1 : cl.ksplit;
   p.y32_slab = cl.y32_slab;
+  p.x_rowmap = cl.x_rowmap;
   for (int b = 0; b < cl.n; ++b) p.owner_idx[b] = cl.owner_idx[b];
   const int sms = device_sm_count();
   const NPlan np = plan_n(cl.d_model, cl.n * std::max(1, cl.ksplit), sms);
@@ -287,13 +531,49 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
   p.nt = np.T;
   p.w_hi = np.w_hi;
   p.h = np.h;
+  const bool fused = cl.lr != nullptr;
+  if (fused) {
+    // every tile must be resident at once: the finish waits on the other K slabs of its tile
+    if (cl.n * np.T * p.ksplit > sms || cl.lr_ctr == nullptr) return cudaErrorInvalidValue;
+    const LowRankRead &q = *cl.lr;
+    p.lr.slots = q.slots;
+    p.lr.slot_elems = q.slot_elems;
+    p.lr.layer_off = q.layer_off;
+    p.lr.R = q.rank;
+    p.lr.Xsrc = q.X;
+    p.lr.resid = q.resid;
+    p.lr.Yout = q.Y;
+    p.lr.u = q.u;
+    p.lr.bu = q.Y32 + (size_t)kMaxKSplit * q.y32_slab;
+    p.lr.ctr = cl.lr_ctr;
+    for (int b = 0; b < q.n; ++b) {
+      p.owner_idx[b] = q.owner_idx[b];
+      p.lr.x_row[b] = q.x_row[b];
+      p.lr.v_row[b] = q.v_row[b];
+      p.lr.y_row[b] = q.y_row[b];
+      p.lr.tail_pos[b] = q.tail_pos[b];
+    }
+    p.Vt = q.Vt;
+    p.tailZ = q.tailZ;
+    p.tailV = q.tailV;
+    p.tz_owner = q.tz_owner;
+    p.tv_owner = q.tv_owner;
+    p.tz_layer = q.tz_layer;
+    p.tv_layer = q.tv_layer;
+  }
   CUtensorMap mX, mW, mD;
-  if (!ptx::make_map_bf16_3d(&mX, cl.X, cl.d_ff, cl.C, cl.n, BK, BM) ||
-      !ptx::make_map_bf16_3d(&mW, cl.w_down, cl.d_ff, cl.d_model, cl.L, BK, np.w_hi) ||
-      !ptx::make_map_bf16_3d(&mD, cl.delta ? cl.slots : cl.w_down, cl.d_ff, cl.d_model,
-                             cl.delta ? (uint64_t)cl.max_slots * cl.L : (uint64_t)cl.L, BK, np.w_hi))
+  const bool xmap_ok = cl.x_rowmap ? cached_map(&mX, cl.X, cl.d_ff, (uint64_t)cl.valid_rows, 1, BK, BM)
+                                   : cached_map(&mX, cl.X, cl.d_ff, cl.C, cl.n, BK, BM);
+  if (!xmap_ok || !cached_map(&mW, cl.w_down, cl.d_ff, cl.d_model, cl.L, BK, np.w_hi) ||
+      !cached_map(&mD, cl.delta ? cl.slots : cl.w_down, cl.d_ff, cl.d_model,
+                  cl.delta ? (uint64_t)cl.max_slots * cl.L : (uint64_t)cl.L, BK, np.w_hi))
     return cudaErrorInvalidValue;
-  return launch_bn<160>(mX, mW, mD, p, s);
+  if (fused) {
+    p.n = (cl.lr->n + BM - 1) / BM;                // tiles index row blocks; members via p.lr
+    p.valid_rows = cl.lr->n;
+    return launch_bn<160, true>(mX, mW, mD, p, s);
+  }
+  return launch_bn<160, false>(mX, mW, mD, p, s);
 }
 
 }  // namespace ttt

@@ -13,6 +13,7 @@ namespace ttt {
 // One owner's host mirror (authoritative for planning; the device tables
 // sel[]/version[] are authoritative for kernels; tttstate_sync reconciles).
 struct OwnerRec {
+  uint64_t stamp = 0;         // group-validation visit mark (μ injectivity check without allocation)
   int idx = -1;               // owner index: slots 2*idx (+0/+1)
   int sel = 0;                // active slot of the pair
   uint64_t version = 0;       // V(r)
@@ -29,7 +30,7 @@ struct OwnerRec {
 
 struct Layout {
   size_t slots = 0, tailZ = 0, tailV = 0, sel = 0, ver = 0, flags = 0, P = 0, tickets = 0;
-  size_t Xg = 0, Y32 = 0, U = 0, total = 0;      // low-rank READ workspace
+  size_t Xg = 0, Y32 = 0, U = 0, Ctr = 0, total = 0;   // low-rank READ workspace
 };
 
 Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt);
@@ -38,6 +39,7 @@ Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt);
 
 struct ttt_pool {
   ttt_shape sh{};
+  uint64_t stamp_epoch = 0;
   int shape_id = 0, placement = 0, max_owners = 0, n_ckpt = 0;
   bool host_only = true;
   unsigned char *arena = nullptr;

@@ -71,8 +71,9 @@ Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt) {
   if (s.backend == TTT_LOW_RANK) {
     const size_t rows = align_up((size_t)max_owners, 128);
     L.Xg = off;  off = align_up(off + rows * s.d_ff * es, 1024);
-    L.Y32 = off; off = align_up(off + (size_t)kMaxKSplit * rows * s.d_model * 4, 1024);
-    L.U = off;   off = align_up(off + (size_t)max_owners * 64 * 4, 1024);
+    L.Y32 = off; off = align_up(off + (size_t)(kMaxKSplit + 1) * rows * s.d_model * 4, 1024);   // + Bᵀu slab
+    L.U = off;   off = align_up(off + (size_t)max_owners * 64 * kMaxLrSeg * 4, 1024);
+    L.Ctr = off; off = align_up(off + (8 + rows / 128 * ((size_t)s.d_model / 16 + 1)) * 4, 1024);
   }
   L.total = off;
   return L;
@@ -116,13 +117,14 @@ ttt_status check_group(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec *> 
   if (g->backend != p->sh.backend || g->shape_id != p->shape_id || g->placement != p->placement)
     return fail(TTT_E_MIXED_KEY, "group key (τ,σ,π) does not match the pool");
   if (g->effect != TTT_READ && g->effect != TTT_WRITE) return fail(TTT_E_INVALID_ARG, "effect");
-  std::unordered_set<uint64_t> seen;
   recs.resize(g->n);
+  const uint64_t epoch = ++p->stamp_epoch;         // μ injective: each record visited once per call
   for (int b = 0; b < g->n; ++b) {
-    if (!seen.insert(g->owner_map[b]).second)
-      return fail(TTT_E_OWNER_COLLISION, "owner " + std::to_string(g->owner_map[b]) + " twice in μ");
     ttt_status st = find_owner(p, g->owner_map[b], &recs[b]);
     if (st != TTT_OK) return st;
+    if (recs[b]->stamp == epoch)
+      return fail(TTT_E_OWNER_COLLISION, "owner " + std::to_string(g->owner_map[b]) + " twice in μ");
+    recs[b]->stamp = epoch;
   }
   return TTT_OK;
 }
@@ -412,6 +414,7 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
     cl.y32_slab = (long long)align_up((size_t)p->max_owners, 128) * sh.d_model;
     lp.ksplit = cl.ksplit;
     lp.y32_slab = cl.y32_slab;
+    lp.ctr = reinterpret_cast<int *>(p->arena + p->lay.Ctr);
     cudaError_t e = launch_lowrank_read(lp, cl, s);
     if (e != cudaSuccess) return cuda_fail(e, "low-rank READ");
     for (int b = 0; b < g->n; ++b) {

@@ -14,6 +14,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import time
+
 import torch
 
 from . import capi
@@ -112,6 +114,7 @@ class Server:
         self.clock = 0
         self.read_events: list = []       # (start, end, launches): events around a step's back-to-back READs
         self.write_events: list = []      # (start, end) around write_commit
+        self.plan_s = 0.0                 # host seconds in NextStep + LegalGroups (P:525's overhead)
 
     def admit(self):
         eng, tr, src = self.eng, self.tr, self.src
@@ -132,6 +135,7 @@ class Server:
     def step(self):
         eng, tr, src, log, stream = self.eng, self.tr, self.src, self.log, self.stream
         pool, owners, clock = eng.pool, self.owners, self.clock
+        t_plan = time.perf_counter()
         events = []
         for s in range(tr.n_streams):                                   # View + NextStep
             if self.pos[s] < tr.n_steps and s not in self.pending:
@@ -155,6 +159,7 @@ class Server:
                 self.pending.add(s)
                 self.ready_at[s] = clock
         groups, rejected = capi.plan_batch(eng.planner, events, clock)  # LegalGroups
+        self.plan_s += time.perf_counter() - t_plan
         if rejected:
             raise RuntimeError(f"planner rejected events of a well-formed trace: {rejected}")
         for g in groups:

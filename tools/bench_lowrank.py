@@ -12,6 +12,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 import torch
 
@@ -26,7 +27,7 @@ from workload import rng  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rank", type=int, default=16)
-    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--layers", type=int, default=12)
     ap.add_argument("--members", type=int, default=128)
     ap.add_argument("--iters", type=int, default=10)
     a = ap.parse_args()
@@ -49,12 +50,14 @@ def main():
     g = capi.Group(capi.READ, owners, backend=capi.LOW_RANK)
     gw = capi.Group(capi.WRITE, owners, backend=capi.LOW_RANK)
     s = torch.cuda.current_stream()
-    ms = []
+    ms, host_us = [], []
     for it in range(a.iters + 2):                    # READ steps (tail fills)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
+        t0 = time.perf_counter()
         for l in range(L):
             capi.read_apply(eng.pool, g, l, X[l], None, V[l], None, Y[l], None, None, s)
+        host_us.append((time.perf_counter() - t0) / L * 1e6)
         e1.record(s)
         capi.tttstate_step_done(eng.pool, g)
         torch.cuda.synchronize()
@@ -75,7 +78,8 @@ def main():
     rms = sorted(ms)[len(ms) // 2]
     rbytes = dm * dff * 2 + B * R * (dff + dm) * 2 + B * (2 * dff + 3 * dm) * 2
     window_ms = 36 * (C * rms + wms)
-    print(json.dumps({"rank": R, "members": B, "read_ms_per_layer": rms, "read_GBps": rbytes / rms / 1e6,
+    print(json.dumps({"rank": R, "members": B, "read_ms_per_layer": rms,
+                      "host_us_per_read_call": sorted(host_us)[len(host_us) // 2], "read_GBps": rbytes / rms / 1e6,
                       "read_frac_hbm": rbytes / rms / 1e6 / peaks["hbm_gbs"], "write_ms_per_layer": wms,
                       "tok_per_s_window_36_layers": B * C / (window_ms / 1e3)}, indent=1))
 
