@@ -188,6 +188,10 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: the prologue above (barriers, TMEM, tensor-map prefetch) overlaps the previous
+  // kernel's tail; everything below may depend on it (X, slots, sel, workspace, counters).
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {                                        // ---------------- TMA producer
@@ -426,9 +430,19 @@ cudaError_t launch_bn(const CUtensorMap &mX, const CUtensorMap &mW, const CUtens
     configured = smem;
   }
   const int tiles = p.n * p.nt * p.ksplit;
-  read_chunk_tc_kernel<BN, LR><<<std::min(device_sm_count(), tiles), LR ? kThreadsLR : kThreads, smem, s>>>(mX, mW, mD, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min(device_sm_count(), tiles));
+  cfg.blockDim = dim3(LR ? kThreadsLR : kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, read_chunk_tc_kernel<BN, LR>, mX, mW, mD, p);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // N-block plan: T blocks per member of widths w_hi (h of them) and w_hi - 16, w_hi ≤ 160,
