@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtttstate.so")
+LIB_PATH = os.environ.get("TTT_LIB_PATH") or os.path.join(_HERE, "lib", "libtttstate.so")   # override: A/B tuning builds
 GEN_PATH = os.path.join(_HERE, "lib", "libttt_gen.so")
 
 if not os.path.exists(LIB_PATH):

@@ -32,8 +32,15 @@ using namespace ptx;
 
 constexpr int BM = 128, BK = 64, kStages = 4;
 constexpr int kThreads = 192;
-constexpr int kUW = 16;                           // fused low-rank mode: u = A x warps per CTA
+#ifndef TTT_LR_UW
+#define TTT_LR_UW 16
+#endif
+constexpr int kUW = TTT_LR_UW;                    // fused low-rank mode: u = A x warps per CTA
 constexpr int kThreadsLR = kThreads + 32 * kUW;
+#ifndef TTT_LR_UB
+#define TTT_LR_UB 12
+#endif
+constexpr int kUB = TTT_LR_UB;                    // fused low-rank: 16-byte loads of A per lane per batch
 
 // fused low-rank READ (NEXT f1) extras: the u = A x stream, the tail append and the finish
 // y = Σ_ks Y32 + Bᵀu (+ resid) run inside the base-GEMM launch (one launch per layer)
@@ -343,12 +350,12 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
       for (int k = uw; k < R; k += kUW) {
         const uint4 *a4 = reinterpret_cast<const uint4 *>(A + (size_t)k * dff);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int v = lane; v < nvec; v += 256) {
-          uint4 a[8];
+        for (int v = lane; v < nvec; v += 32 * kUB) {
+          uint4 a[kUB];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) a[q] = v + 32 * q < nvec ? ld_stream(a4 + v + 32 * q) : make_uint4(0u, 0u, 0u, 0u);
+          for (int q = 0; q < kUB; ++q) a[q] = v + 32 * q < nvec ? ld_stream(a4 + v + 32 * q) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
+          for (int q = 0; q < kUB; ++q) {
             if (v + 32 * q < nvec) {
               const uint4 z = xs_lr[v + 32 * q];
               float &ac = acc[q & 3];
