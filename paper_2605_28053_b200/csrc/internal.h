@@ -35,6 +35,7 @@ struct ReadParams {
   float eta;
   int *fail_flag;
   int order;                     // task order: 0 CTA-major, 1 SM-interleaved (balanced bytes per SM)
+  int kc;                        // > 0: tensor-core base (bf16), Pbase holds kc K-chunk slabs [kc][8][d_model]
 };
 
 // a5: chunk update of one layer for every member (shadow slot <- ΔW_v + η VᵀZ).
@@ -118,6 +119,7 @@ bool read_chunk_supported(int d_model, int d_ff, int C);
 cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s);
 cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s);
 bool read_decode_fits(int n, int d_model, int d_ff, int esize);
+int read_decode_mma_chunks(int dtype, int d_ff);   // > 0: the bf16 tensor-core-base READ applies (its K chunks)
 cudaError_t launch_write_simt(int dtype, const WriteParams &p, cudaStream_t s);
 cudaError_t launch_write_tc(const WriteParams &p, cudaStream_t s);   // bf16, tcgen05
 bool write_tc_supported(int d_model, int d_ff, int C);

@@ -308,6 +308,228 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
   if (FUSE && Upd<T>::bad(expmax)) atomicOr(p.fail_flag, 1);
 }
 
+// ---------------------------------------------------------------------------
+// bf16 READ with the shared base product on tensor cores.  The base term X·W_downᵀ for the
+// group's ≤ 8 members is a real (skinny) GEMM — N = 8 members — so it runs as
+// mma.sync.m16n8k16 (bf16 in, fp32 accumulate): a base task is 16 rows of W_down × a
+// 512-wide K chunk (16 KB, the size of a ΔW row task), the A fragment comes straight from the
+// 16-byte streaming loads (K is permuted identically on both operands, so no shuffles) and
+// the B fragment is one 16-byte read of the staged x.  That replaces 64 FHFMA + 8 LDS per
+// 16 bytes of W_down with ¼ MMA, which the SIMT version spent ~10 % of the launch on.  The
+// per-member ΔW rows (GEMVs) stay SIMT.  Row i combines, in a fixed order, the K-chunk
+// partials of the base and the member's ΔW partial once all n + KC tasks of row i arrived.
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+constexpr int kMmaThreads = 1024, kMmaChunkVec = 64;   // 512 bf16 of K per base task
+
+__host__ __device__ inline int mma_nvp(int nvec) { return (nvec + 127) / 128 * 128; }
+
+template <bool FUSE>
+__global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const ReadParams p) {
+  constexpr int kWarps = kMmaThreads / 32;
+  using E = Elem<__nv_bfloat16>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint4 *xs = reinterpret_cast<uint4 *>(smem_raw);      // [8][nvp] member x rows, zero padded
+  __shared__ const uint4 *s_row0[kMaxReadMembers + 1];
+  __shared__ uint4 *s_dst0[kMaxReadMembers];
+
+  const int n = p.n, dff = p.d_ff, dm = p.d_model, nvec = dff / 8, nvp = mma_nvp(nvec);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, tq = lane & 3;
+  const int KC = p.kc, n_base = (dm + 15) / 16 * KC, n_tasks = n_base + n * dm;
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int stride = gridDim.x * kWarps;
+  int t = p.order ? warp * gridDim.x + blockIdx.x : blockIdx.x * kWarps + warp;
+  const uint4 *W = static_cast<const uint4 *>(p.w_down_l);
+
+  // base task tt: rows r0 = 16·(tt / KC) (+g, +g+8) × vectors {8j + tq, 8j + 4 + tq} of K chunk tt % KC
+  auto load_base = [&](uint4 (&buf)[4], int tt, int j) {
+    const int rb = tt / KC, kc = tt - rb * KC, r = rb * 16 + g, v0 = kc * kMmaChunkVec + 8 * j + tq;
+    const uint4 *q = W + (size_t)r * nvec + v0;
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    buf[0] = (r < dm && v0 < nvec) ? ld_stream(q) : z;
+    buf[1] = (r < dm && v0 + 4 < nvec) ? ld_stream(q + 4) : z;
+    buf[2] = (r + 8 < dm && v0 < nvec) ? ld_stream(q + 8 * (size_t)nvec) : z;
+    buf[3] = (r + 8 < dm && v0 + 4 < nvec) ? ld_stream(q + 8 * (size_t)nvec + 4) : z;
+  };
+  // ΔW task: 4 × 32 lanes of one row
+  auto load_delta = [&](uint4 (&buf)[4], const uint4 *rw, int v0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) buf[u] = v0 + 32 * u < nvec ? ld_stream(rw + v0 + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
+  };
+
+  uint4 cur[4], nxt[4];
+  const bool early = t < n_base;                  // base tasks read only W_down before the wait
+  if (early) load_base(cur, t, 0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tid <= n) {
+    if (tid == 0) {
+      s_row0[0] = W;
+    } else {
+      const int o = p.owner_idx[tid - 1];
+      s_row0[tid] = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.slots) +
+                                                    (2LL * o + p.sel[o]) * p.slot_elems + p.layer_off);
+      if (FUSE)
+        s_dst0[tid - 1] = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(const_cast<void *>(p.slots)) +
+                                                    (2LL * o + 1 - p.sel[o]) * p.slot_elems + p.layer_off);
+    }
+  }
+  __syncthreads();
+  const uint4 *row = nullptr;
+  int v = lane;
+  if (!early && t < n_tasks) {
+    const int td = t - n_base, m = td / dm;
+    row = s_row0[m + 1] + (size_t)(td - m * dm) * nvec;
+    load_delta(cur, row, v);
+  }
+  for (int idx = tid; idx < kMaxReadMembers * nvp; idx += kMmaThreads) {   // x rows; zero pad / absent members
+    const int b = idx / nvp, vv = idx - b * nvp;
+    xs[idx] = (b < n && vv < nvec)
+                  ? reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff)[vv]
+                  : make_uint4(0u, 0u, 0u, 0u);
+  }
+  {                                               // a4 — TailBufferUpdate, spread over every CTA
+    const int zq = n * nvec, gtid = blockIdx.x * kMmaThreads + tid, gsz = gridDim.x * kMmaThreads;
+    for (int idx = gtid; idx < zq; idx += gsz) {
+      const int b = idx / nvec, vv = idx - b * nvec, o = p.owner_idx[b];
+      reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.tailZ) + o * p.tz_owner + p.tz_layer +
+                                (size_t)p.tail_pos[b] * dff)[vv] =
+          reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff)[vv];
+    }
+    for (int idx = gtid; idx < n * dm; idx += gsz) {
+      const int b = idx / dm, ii = idx - b * dm, o = p.owner_idx[b];
+      (static_cast<__nv_bfloat16 *>(p.tailV) + o * p.tv_owner + p.tv_layer + (size_t)p.tail_pos[b] * dm)[ii] =
+          (static_cast<const __nv_bfloat16 *>(p.Vt) + (size_t)p.v_row[b] * dm)[ii];
+    }
+  }
+  __syncthreads();
+  if (t >= n_tasks) return;
+
+  const int target = n + KC;                      // arrivals per output row
+  auto combine = [&](int i) {                     // y_b[i] = Σ_kc base partials + ΔW_b partial (fixed order)
+    if (lane < n) {
+      float y = 0.f;
+      for (int kc = 0; kc < KC; ++kc) y += __ldcg(p.Pbase + ((size_t)kc * kMaxReadMembers + lane) * dm + i);
+      y += __ldcg(p.Pdelta + (size_t)lane * dm + i);
+      if (p.resid) y += E::to_f(static_cast<const __nv_bfloat16 *>(p.resid)[(size_t)p.y_row[lane] * dm + i]);
+      static_cast<__nv_bfloat16 *>(p.Y)[(size_t)p.y_row[lane] * dm + i] = E::from_f(y);
+    }
+    if (lane == 0) p.tickets[i] = 0;              // self-reset for the next launch
+  };
+
+  // ---- phase 1: base tasks (16 rows × 512 of K on mma.sync), batches double-buffered
+  while (t < n_base) {
+    const int rb = t / KC, kc = t - rb * KC, r0 = rb * 16;
+    const int nb = min(8, (nvec - kc * kMmaChunkVec + 7) / 8);
+    const uint4 *xg = xs + (size_t)g * nvp + kc * kMmaChunkVec + tq;
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < nb; ++j) {
+      if (j + 1 < nb) load_base(nxt, t, j + 1);
+      const uint4 b0 = xg[8 * j], b1 = xg[8 * j + 4];
+      mma_bf16_16816(c, cur[0].x, cur[2].x, cur[0].y, cur[2].y, b0.x, b0.y);
+      mma_bf16_16816(c, cur[0].z, cur[2].z, cur[0].w, cur[2].w, b0.z, b0.w);
+      mma_bf16_16816(c, cur[1].x, cur[3].x, cur[1].y, cur[3].y, b1.x, b1.y);
+      mma_bf16_16816(c, cur[1].z, cur[3].z, cur[1].w, cur[3].w, b1.z, b1.w);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+    }
+    const int nt = t + stride;                    // prefetch the next task's first batch
+    if (nt < n_base) load_base(cur, nt, 0);
+    else if (nt < n_tasks) {
+      const int td = nt - n_base, m = td / dm;
+      row = s_row0[m + 1] + (size_t)(td - m * dm) * nvec;
+      load_delta(cur, row, lane);
+    }
+    // c0,c1: row r0+g, members 2tq, 2tq+1; c2,c3: row r0+g+8
+    {
+      const int r = r0 + g;
+      float *P = p.Pbase + ((size_t)kc * kMaxReadMembers + 2 * tq) * dm;
+      if (r < dm) {
+        P[r] = c[0];
+        P[dm + r] = c[1];
+      }
+      if (r + 8 < dm) {
+        P[r + 8] = c[2];
+        P[dm + r + 8] = c[3];
+      }
+    }
+    __syncwarp();
+    __threadfence();
+    int last = 0;
+    if (lane < 16 && r0 + lane < dm) last = atomicAdd(p.tickets + r0 + lane, 1) == target - 1;
+    unsigned mask = __ballot_sync(0xffffffffu, last);
+    if (mask) __threadfence();
+    while (mask) {
+      const int l = __ffs(mask) - 1;
+      mask &= mask - 1;
+      combine(r0 + l);
+    }
+    t = nt;
+  }
+  if (t >= n_tasks) return;
+
+  // ---- phase 2: ΔW rows (SIMT GEMVs, FHFMA), the next batch always in flight
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  uint32_t expmax = 0;
+  while (true) {
+    int nv = v + 128, nt = t;
+    const uint4 *nrow = row;
+    const bool task_end = nv >= nvec;
+    if (task_end) {
+      nt = t + stride;
+      nv = lane;
+      if (nt < n_tasks) {
+        const int td = nt - n_base, m = td / dm;
+        nrow = s_row0[m + 1] + (size_t)(td - m * dm) * nvec;
+      }
+    }
+    const bool more = nt < n_tasks;
+    if (more) load_delta(nxt, nrow, nv);
+    const int td = t - n_base, m = td / dm, i = td - m * dm;
+    const uint4 *xb = xs + (size_t)m * nvp + v;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) E::dot(acc[u], cur[u], xb[32 * u]);
+    if (FUSE) {
+      const float ev = p.eta * E::to_f(static_cast<const __nv_bfloat16 *>(p.Vt)[(size_t)p.v_row[m] * dm + i]);
+      uint4 *drow = s_dst0[m] + (size_t)i * nvec;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (v + 32 * u < nvec) drow[v + 32 * u] = Upd<__nv_bfloat16>::apply(cur[u], xb[32 * u], ev, expmax);
+    }
+    if (task_end) {
+      float sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      if (lane == 0) p.Pdelta[(size_t)m * dm + i] = sum;
+      __syncwarp();
+      int old = 0;
+      if (lane == 0) {
+        __threadfence();
+        old = atomicAdd(p.tickets + i, 1);
+      }
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (old == target - 1) {
+        __threadfence();
+        combine(i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = 0.f;
+    }
+    if (!more) break;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+    v = nv;
+    row = nrow;
+    t = nt;
+  }
+  if (FUSE && Upd<__nv_bfloat16>::bad(expmax)) atomicOr(p.fail_flag, 1);
+}
+
 size_t smem_bytes(int n, int d_ff, int esize) { return (size_t)n * d_ff * esize; }
 
 template <typename T, int TH, int U, bool FUSE>
@@ -373,7 +595,47 @@ bool read_decode_fits(int n, int d_model, int d_ff, int esize) {
   return smem_bytes(n, d_ff, esize) <= 220 * 1024;
 }
 
+namespace {
+template <bool FUSE>
+cudaError_t launch_mma(const ReadParams &p, cudaStream_t s) {
+  const size_t smem = (size_t)kMaxReadMembers * mma_nvp(p.d_ff / 8) * 16;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(read_decode_mma_kernel<FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<size_t>(smem, 48 * 1024));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  static const bool pdl = !getenv("TTT_PDL") || atoi(getenv("TTT_PDL")) != 0;
+  static const int order = getenv("TTT_READ_ORDER") ? atoi(getenv("TTT_READ_ORDER")) : 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(device_sm_count());
+  cfg.blockDim = dim3(kMmaThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ReadParams q = p;
+  q.order = order;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, read_decode_mma_kernel<FUSE>, q);
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+}  // namespace
+
+int read_decode_mma_chunks(int dtype, int d_ff) {
+  static const bool on = !getenv("TTT_READ_MMA") || atoi(getenv("TTT_READ_MMA")) != 0;
+  if (!on || dtype != 1 || d_ff % 8) return 0;
+  if ((size_t)kMaxReadMembers * mma_nvp(d_ff / 8) * 16 > 220 * 1024) return 0;
+  return (d_ff / 8 + kMmaChunkVec - 1) / kMmaChunkVec;
+}
+
 cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s) {
+  if (p.kc > 0) return p.fuse ? launch_mma<true>(p, s) : launch_mma<false>(p, s);
   if (dtype == 1) return launch_t<__nv_bfloat16>(p, s);
   return launch_t<float>(p, s);
 }

@@ -66,7 +66,8 @@ Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt) {
   L.sel = off;     off = align_up(off + (size_t)max_owners * 4, 256);
   L.ver = off;     off = align_up(off + (size_t)max_owners * 8, 256);
   L.flags = off;   off = align_up(off + 64, 256);
-  L.P = off;       off = align_up(off + 2 * (size_t)kMaxReadMembers * s.d_model * 4, 256);
+  // READ partials: base K-chunk slabs [kc][8][d_model] (kc ≤ ⌈d_ff/512⌉) + ΔW [8][d_model]
+  L.P = off;       off = align_up(off + ((size_t)(s.d_ff + 511) / 512 + 1) * kMaxReadMembers * s.d_model * 4, 256);
   L.tickets = off; off = align_up(off + (size_t)s.d_model * 4, 1024);
   if (s.backend == TTT_LOW_RANK) {
     const size_t rows = align_up((size_t)max_owners, 128);
@@ -440,8 +441,9 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
     rp.tz_owner = p->tz_owner; rp.tv_owner = p->tv_owner;
     rp.tz_layer = (long long)layer * sh.chunk * sh.d_ff;
     rp.tv_layer = (long long)layer * sh.chunk * sh.d_model;
+    rp.kc = read_decode_mma_chunks(sh.dtype, sh.d_ff);
     rp.Pbase = reinterpret_cast<float *>(p->arena + p->lay.P);
-    rp.Pdelta = rp.Pbase + (size_t)kMaxReadMembers * sh.d_model;
+    rp.Pdelta = rp.Pbase + (size_t)std::max(1, rp.kc) * kMaxReadMembers * sh.d_model;
     rp.tickets = reinterpret_cast<int *>(p->arena + p->lay.tickets);
     rp.n = std::min(per, g->n - b0);
     rp.d_model = sh.d_model; rp.d_ff = sh.d_ff;
