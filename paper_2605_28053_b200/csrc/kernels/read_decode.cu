@@ -473,24 +473,27 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
   }
   if (t >= n_tasks) return;
 
-  // ---- phase 2: ΔW rows (SIMT GEMVs, FHFMA), the next batch always in flight
+  // ---- phase 2: ΔW rows (SIMT GEMVs, FHFMA), the next batch always in flight; the task's
+  // (member, row) are decoded once per task, not per batch
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
   uint32_t expmax = 0;
+  int m = (t - n_base) / dm, i = (t - n_base) - m * dm;
   while (true) {
-    int nv = v + 128, nt = t;
+    int nv = v + 128, nt = t, nm = m, ni = i;
     const uint4 *nrow = row;
     const bool task_end = nv >= nvec;
     if (task_end) {
       nt = t + stride;
       nv = lane;
       if (nt < n_tasks) {
-        const int td = nt - n_base, m = td / dm;
-        nrow = s_row0[m + 1] + (size_t)(td - m * dm) * nvec;
+        const int td = nt - n_base;
+        nm = td / dm;
+        ni = td - nm * dm;
+        nrow = s_row0[nm + 1] + (size_t)ni * nvec;
       }
     }
     const bool more = nt < n_tasks;
     if (more) load_delta(nxt, nrow, nv);
-    const int td = t - n_base, m = td / dm, i = td - m * dm;
     const uint4 *xb = xs + (size_t)m * nvp + v;
 #pragma unroll
     for (int u = 0; u < 4; ++u) E::dot(acc[u], cur[u], xb[32 * u]);
@@ -526,6 +529,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
     v = nv;
     row = nrow;
     t = nt;
+    m = nm;
+    i = ni;
   }
   if (FUSE && Upd<__nv_bfloat16>::bad(expmax)) atomicOr(p.fail_flag, 1);
 }
