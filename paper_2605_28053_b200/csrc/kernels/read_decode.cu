@@ -414,8 +414,17 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
   auto combine = [&](int i) {                     // y_b[i] = Σ_kc base partials + ΔW_b partial (fixed order)
     if (lane < n) {
       float y = 0.f;
-      for (int kc = 0; kc < KC; ++kc) y += __ldcg(p.Pbase + ((size_t)kc * kMaxReadMembers + lane) * dm + i);
-      y += __ldcg(p.Pdelta + (size_t)lane * dm + i);
+      const float dlt = __ldcg(p.Pdelta + (size_t)lane * dm + i);
+      for (int kc0 = 0; kc0 < KC; kc0 += 8) {     // 8 partial loads in flight, summed in kc order
+        float part[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          part[e] = kc0 + e < KC ? __ldcg(p.Pbase + ((size_t)(kc0 + e) * kMaxReadMembers + lane) * dm + i) : 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (kc0 + e < KC) y += part[e];
+      }
+      y += dlt;
       if (p.resid) y += E::to_f(static_cast<const __nv_bfloat16 *>(p.resid)[(size_t)p.y_row[lane] * dm + i]);
       static_cast<__nv_bfloat16 *>(p.Y)[(size_t)p.y_row[lane] * dm + i] = E::from_f(y);
     }
@@ -458,8 +467,9 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
         P[dm + r + 8] = c[3];
       }
     }
+    __syncwarp();                                 // the warp's partials, then one release fence
+    if (lane == 0) __threadfence();
     __syncwarp();
-    __threadfence();
     int last = 0;
     if (lane < 16 && r0 + lane < dm) last = atomicAdd(p.tickets + r0 + lane, 1) == target - 1;
     unsigned mask = __ballot_sync(0xffffffffu, last);
