@@ -378,7 +378,7 @@ def main():
                        "tokens_per_step_per_gpu": window * N_STREAMS},
             "e2e": e2e,
             "gpu_launches": n_launch,
-            "roofline": {"kernel": "read_decode_kernel (a3+a4 READ)", "bound": "hbm", "achieved": achieved,
+            "roofline": {"kernel": "read_decode_mma_kernel (a3+a4 READ: W_down base on mma.sync, dW rows SIMT)", "bound": "hbm", "achieved": achieved,
                          "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "alg_bytes_per_launch": read_bytes, "avg_launch_ms": read_avg,
                          "launches_timed": len(read_ms), "peak_source": "MEASURED_PEAKS.json hbm_gbs",
