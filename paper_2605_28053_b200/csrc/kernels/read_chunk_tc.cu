@@ -86,6 +86,12 @@ __device__ __forceinline__ void fma_bf16x2(float &acc, uint32_t a, uint32_t z) {
       : "+f"(acc)
       : "r"(a), "r"(z));
 }
+// named barrier among a subset of warps (non-.aligned form: callers may arrive diverged,
+// e.g. after the single spinning thread of the finish gate)
+template <int ID, int COUNT>
+__device__ __forceinline__ void named_bar() {
+  asm volatile("barrier.sync %0, %1;" ::"n"(ID), "n"(COUNT) : "memory");
+}
 __device__ __forceinline__ int ld_volatile(const int *q) {
   int v;
   asm volatile("ld.volatile.global.b32 %0, [%1];" : "=r"(v) : "l"(q));
@@ -97,7 +103,7 @@ __device__ __forceinline__ int ld_volatile(const int *q) {
 // 8 outputs per item with the R loads of u and B issued 8 at a time.
 template <int BN>
 __device__ __forceinline__ void lr_finish(const ChunkParams &p, int b, int j, int ks, int n0, int width, int ft) {
-  asm volatile("bar.sync 2, %0;" ::"n"(128 + 32 * kUW) : "memory");
+  named_bar<2, 128 + 32 * kUW>();
   const LrFused &lr = p.lr;
   const int KS = p.ksplit;
   const int rows = min(BM, p.valid_rows - b * BM), r_lo = rows * ks / KS, r_hi = rows * (ks + 1) / KS;
@@ -308,7 +314,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(t_empty);
       if (LR) {                                    // f1: arm the finish of this tile
-        asm volatile("bar.sync 1, 128;" ::: "memory");   // this CTA's slab is written
+        named_bar<1, 128>();                       // this CTA's slab is written
         if (et == 0) {
           int *tick = p.lr.ctr + 2 + b * nt + j;
           __threadfence();
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
                                                         (size_t)lr.x_row[m] * dff);
       uint4 *tz = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.tailZ) + o * p.tz_owner + p.tz_layer +
                                             (size_t)lr.tail_pos[m] * dff);
-      asm volatile("bar.sync 3, %0;" ::"n"(32 * kUW) : "memory");   // previous member's rows done
+      named_bar<3, 32 * kUW>();   // previous member's rows done
       for (int v = ut; v < nvec; v += 32 * kUW) {    // stage x_m; a4: append z_m
         const uint4 z = x4[v];
         xs_lr[v] = z;
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
                                               (size_t)lr.tail_pos[m] * dm);
         for (int v = ut; v < dm / 8; v += 32 * kUW) tv[v] = vs[v];
       }
-      asm volatile("bar.sync 3, %0;" ::"n"(32 * kUW) : "memory");   // x_m staged
+      named_bar<3, 32 * kUW>();   // x_m staged
       const __nv_bfloat16 *A = static_cast<const __nv_bfloat16 *>(lr.slots) + (2LL * o + p.sel[o]) * lr.slot_elems +
                                lr.layer_off;
       for (int k = uw; k < R; k += kUW) {
@@ -369,7 +375,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
         for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
         if (lane == 0) us_lr[k] = sum;
       }
-      asm volatile("bar.sync 3, %0;" ::"n"(32 * kUW) : "memory");   // u_m complete (shared memory)
+      named_bar<3, 32 * kUW>();   // u_m complete (shared memory)
       // Bᵀu_m: 8 outputs per thread, the R rows of B_m streamed 8 loads at a time
       const uint4 *B4 = reinterpret_cast<const uint4 *>(A + (size_t)R * dff);
       for (int i8 = ut; i8 < dm / 8; i8 += 32 * kUW) {
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
         o4[0] = make_float4(y[0], y[1], y[2], y[3]);
         o4[1] = make_float4(y[4], y[5], y[6], y[7]);
       }
-      asm volatile("bar.sync 3, %0;" ::"n"(32 * kUW) : "memory");   // Bᵀu_m written
+      named_bar<3, 32 * kUW>();   // Bᵀu_m written
       if (ut == 0) {
         __threadfence();
         atomicAdd(lr.ctr, 1);
@@ -407,6 +413,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
     lr_finish<BN>(p, b, j, blockIdx.x % KS, n0_of(j), width_of(j), 128 + uw * 32 + lane);
   }
   tc_fence_before();
+  __syncwarp();                                    // warp 0: the producer lane rejoins its warp
   __syncthreads();
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
   if (LR && threadIdx.x == 0) {                    // the last CTA out re-arms the counters
