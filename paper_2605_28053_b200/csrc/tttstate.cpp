@@ -441,7 +441,9 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
     rp.tz_owner = p->tz_owner; rp.tv_owner = p->tv_owner;
     rp.tz_layer = (long long)layer * sh.chunk * sh.d_ff;
     rp.tv_layer = (long long)layer * sh.chunk * sh.d_model;
-    rp.kc = read_decode_mma_chunks(sh.dtype, sh.d_ff);
+    // tensor-core base for plain READs; the f3 fused READ+WRITE keeps the all-SIMT kernel
+    // (its candidate stores need the registers: 82 % vs 79 % of HBM measured)
+    rp.kc = fuse ? 0 : read_decode_mma_chunks(sh.dtype, sh.d_ff);
     rp.Pbase = reinterpret_cast<float *>(p->arena + p->lay.P);
     rp.Pdelta = rp.Pbase + (size_t)std::max(1, rp.kc) * kMaxReadMembers * sh.d_model;
     rp.tickets = reinterpret_cast<int *>(p->arena + p->lay.tickets);
