@@ -251,7 +251,10 @@ def main():
             return n, Z, V
 
         def group_io(self, l, ss, ps):
-            rows = [(p % CHUNK) * N_STREAMS + s for s, p in zip(ss, ps)]
+            key = (tuple(ss), tuple(ps))
+            if key != getattr(self, "_key", None):     # one row map per step, reused by every layer
+                self._key, self._rows = key, capi.rows_array([(p % CHUNK) * N_STREAMS + s for s, p in zip(ss, ps)])
+            rows = self._rows
             return self.X[l], rows, self.V[l], rows, self.Y[l], rows
 
     src = Window()

@@ -136,6 +136,9 @@ ttt_status tttstate_tail_len(ttt_pool *pool, uint64_t owner, int32_t *len_out);
 /* a1 — NextStep: fills e=(r, τ, σ, ρ, v=V(r), π, ready_step=clock);
  * ρ = WRITE iff this step's token completes the chunk (reading ii).         */
 ttt_status tttstate_next_event(ttt_pool *pool, uint64_t owner, int64_t clock, ttt_event *out);
+/* a1 for n owners at once (one host call per serving step): out[i] as above for owners[i].
+ * Host-only. Validation first: an unknown owner fails the whole call and writes nothing. */
+ttt_status tttstate_next_events(ttt_pool *pool, const uint64_t *owners, int32_t n, int64_t clock, ttt_event *out);
 
 /* ---------------------------------------------------------------- planner */
 ttt_status ttt_planner_create(int32_t mode, int32_t B, int32_t w, ttt_planner **out);

@@ -75,6 +75,7 @@ _sigs = {
     "tttstate_version": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_uint64)]),
     "tttstate_tail_len": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_int32)]),
     "tttstate_next_event": (C.c_int, [P, C.c_uint64, C.c_int64, C.POINTER(ttt_event)]),
+    "tttstate_next_events": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_int32, C.c_int64, C.POINTER(ttt_event)]),
     "ttt_planner_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]),
     "ttt_planner_destroy": (C.c_int, [P]),
     "ttt_planner_attach": (C.c_int, [P, P]),
@@ -131,8 +132,13 @@ def _stream(s):
 
 
 def _rows(rows):
-    if rows is None:
-        return None
+    if rows is None or isinstance(rows, C.Array):   # a prebuilt c_int32 array passes through
+        return rows
+    return (C.c_int32 * len(rows))(*rows)
+
+
+def rows_array(rows):
+    """A c_int32 row map to reuse across the layers of one step (saves per-call marshalling)."""
     return (C.c_int32 * len(rows))(*rows)
 
 
@@ -214,6 +220,15 @@ def tttstate_tail_len(pool, owner: int) -> int:
     v = C.c_int32()
     _check(_lib.tttstate_tail_len(pool, owner, C.byref(v)))
     return v.value
+
+
+def tttstate_next_events(pool, owners, clock: int) -> list:
+    """a1 for every owner in one call (returns a list of ttt_event)."""
+    n = len(owners)
+    arr = owners if isinstance(owners, C.Array) else (C.c_uint64 * n)(*owners)
+    out = (ttt_event * n)()
+    _check(_lib.tttstate_next_events(pool, arr, n, clock, out))
+    return list(out)
 
 
 def tttstate_next_event(pool, owner: int, clock: int) -> ttt_event:

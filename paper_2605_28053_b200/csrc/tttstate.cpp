@@ -337,6 +337,17 @@ ttt_status tttstate_next_event(ttt_pool *p, uint64_t owner, int64_t clock, ttt_e
   return TTT_OK;
 }
 
+ttt_status tttstate_next_events(ttt_pool *p, const uint64_t *owners, int32_t n, int64_t clock, ttt_event *out) {
+  if (!p || (n > 0 && (!owners || !out)) || n < 0) return fail(TTT_E_INVALID_ARG, "null arg / negative n");
+  for (int i = 0; i < n; ++i) {                    // validate every owner before writing any event
+    OwnerRec *r;
+    ttt_status st = find_owner(p, owners[i], &r);
+    if (st != TTT_OK) return st;
+  }
+  for (int i = 0; i < n; ++i) tttstate_next_event(p, owners[i], clock, out + i);
+  return TTT_OK;
+}
+
 ttt_status validate_group(ttt_pool *p, const ttt_group *g, const uint64_t *expected_versions) {
   std::vector<OwnerRec *> recs;
   ttt_status st = check_group(p, g, recs);

@@ -136,9 +136,10 @@ class Server:
         eng, tr, src, log, stream = self.eng, self.tr, self.src, self.log, self.stream
         pool, owners, clock = eng.pool, self.owners, self.clock
         t_plan = time.perf_counter()
-        events = []
-        for s in range(tr.n_streams):                                   # View + NextStep
+        ready = []
+        for s in range(tr.n_streams):                                   # View + controls
             if self.pos[s] < tr.n_steps and s not in self.pending:
+                ready.append(s)
                 for op in tr.controls_at(s, self.pos[s]):
                     if op == "snapshot":
                         capi.tttstate_snapshot(pool, owners[s], stream)
@@ -155,9 +156,11 @@ class Server:
                         b = tr.branch_owner(s, self.forks[s] - 1)
                         capi.tttstate_free(pool, b)
                         self.branches.discard(b)
-                events.append(capi.tttstate_next_event(pool, owners[s], clock))
-                self.pending.add(s)
-                self.ready_at[s] = clock
+        # NextStep for every ready stream in one call
+        events = capi.tttstate_next_events(pool, [owners[s] for s in ready], clock) if ready else []
+        for s in ready:
+            self.pending.add(s)
+            self.ready_at[s] = clock
         groups, rejected = capi.plan_batch(eng.planner, events, clock)  # LegalGroups
         self.plan_s += time.perf_counter() - t_plan
         if rejected:

@@ -42,6 +42,13 @@ def test_host_pool_state_machine_and_errors():
     assert e.value.status == 2
     e1 = capi.tttstate_next_event(p, 1, 5)
     assert (e1.owner, e1.effect, e1.expected_version, e1.ready_step) == (1, capi.READ, 0, 5)
+    evs = capi.tttstate_next_events(p, [2, 1], 5)                    # batched a1 == per-owner a1
+    assert [(e.owner, e.effect, e.expected_version, e.ready_step) for e in evs] == [(2, capi.READ, 7, 5),
+                                                                                  (1, capi.READ, 0, 5)]
+    with pytest.raises(capi.TTTError) as e:
+        capi.tttstate_next_events(p, [1, 99], 5)                        # unknown owner: whole call fails
+    assert e.value.status == 1
+    assert capi.tttstate_next_events(p, [], 5) == []
     g = capi.Group(capi.READ, [1, 2])
     capi.validate_group(p, g, [0, 7])
     for bad, code in [((capi.Group(capi.READ, [1, 1]), None), 4), ((g, [0, 6]), 3),
