@@ -1,0 +1,29 @@
+"""The alternative kernel paths, selected by environment at library load, run the same
+parity suites in a subprocess: the all-SIMT bf16 decode READ (used when the tensor-core-base
+kernel's shared-memory staging does not fit, e.g. d_ff > 14,080), the three-launch low-rank
+READ (used when a fused launch would not fit one CTA per tile), and the serial-order READ."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(env_extra, target):
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", target], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=850)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("env,target", [
+    ({"TTT_READ_MMA": "0"}, "tests/test_gpu_parity.py"),
+    ({"TTT_READ_MMA": "0", "TTT_READ_ORDER": "0"}, "tests/test_gpu_paper_dims.py"),
+    ({"TTT_LR_FUSED": "0"}, "tests/test_gpu_lowrank.py"),
+])
+def test_alternative_paths_parity(env, target):
+    _run(env, target)
