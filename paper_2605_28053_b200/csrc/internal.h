@@ -35,6 +35,7 @@ struct ReadParams {
   float eta;
   int *fail_flag;
   int order;                     // task order: 0 CTA-major, 1 SM-interleaved (balanced bytes per SM)
+  int dyn;                       // per-CTA dynamic task hand-out (SM-interleaved order only)
   int kc;                        // > 0: tensor-core base (bf16), Pbase holds kc K-chunk slabs [kc][8][d_model]
 };
 

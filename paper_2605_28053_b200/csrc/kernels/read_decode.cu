@@ -338,6 +338,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
   uint4 *xs = reinterpret_cast<uint4 *>(smem_raw);      // [8][nvp] member x rows, zero padded
   __shared__ const uint4 *s_row0[kMaxReadMembers + 1];
   __shared__ uint4 *s_dst0[kMaxReadMembers];
+  __shared__ int s_next;                                  // per-CTA dynamic task counter (p.dyn)
 
   const int n = p.n, dff = p.d_ff, dm = p.d_model, nvec = dff / 8, nvp = mma_nvp(nvec);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, tq = lane & 3;
@@ -345,6 +346,18 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
   asm volatile("griddepcontrol.launch_dependents;");
   const int stride = gridDim.x * kWarps;
   int t = p.order ? warp * gridDim.x + blockIdx.x : blockIdx.x * kWarps + warp;
+  // Next task of this warp. Static: t + stride. Dynamic (p.dyn, SM-interleaved order): the
+  // CTA's task list t ≡ blockIdx.x (mod grid) is handed out by a shared-memory counter, so
+  // warps that run ahead take more tasks and the CTA's warps finish together — a static split
+  // left a ~15 µs tail where the last warps streamed alone (per-warp bandwidth is latency-bound).
+  auto next_task = [&](int tt) -> int {
+    if (!p.dyn) return tt + stride;
+    int k = 0;
+    if (lane == 0) k = atomicAdd(&s_next, 1);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    return (int)blockIdx.x + (int)gridDim.x * k;
+  };
+  if (tid == 0) s_next = kWarps;
   const uint4 *W = static_cast<const uint4 *>(p.w_down_l);
 
   // base task tt: rows r0 = 16·(tt / KC) (+g, +g+8) × vectors {8j + tq, 8j + 4 + tq} of K chunk tt % KC
@@ -447,7 +460,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
 #pragma unroll
       for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
     }
-    const int nt = t + stride;                    // prefetch the next task's first batch
+    const int nt = next_task(t);                  // prefetch the next task's first batch
     if (nt < n_base) load_base(cur, nt, 0);
     else if (nt < n_tasks) {
       const int td = nt - n_base, m = td / dm;
@@ -623,6 +636,7 @@ cudaError_t launch_mma(const ReadParams &p, cudaStream_t s) {
   }
   static const bool pdl = !getenv("TTT_PDL") || atoi(getenv("TTT_PDL")) != 0;
   static const int order = getenv("TTT_READ_ORDER") ? atoi(getenv("TTT_READ_ORDER")) : 1;
+  static const int dyn = getenv("TTT_READ_DYN") ? atoi(getenv("TTT_READ_DYN")) : 1;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(device_sm_count());
   cfg.blockDim = dim3(kMmaThreads);
@@ -635,6 +649,7 @@ cudaError_t launch_mma(const ReadParams &p, cudaStream_t s) {
   cfg.numAttrs = 1;
   ReadParams q = p;
   q.order = order;
+  q.dyn = order == 1 ? dyn : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, read_decode_mma_kernel<FUSE>, q);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
