@@ -208,6 +208,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: only the prologue above overlaps the previous kernel (the layer's READ or WRITE);
+  // the tails, slots and the active-slot table are read after the wait.
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -404,9 +408,19 @@ cudaError_t launch_write_tc(const WriteParams &wp, cudaStream_t s) {
   }
   const int tiles = wp.n * (wp.d_model / BM) * (wp.d_ff / BN);
   const int grid = std::min(device_sm_count(), tiles);
-  write_tc_kernel<<<grid, kThreads, smem, s>>>(mV, mZ, mW, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, write_tc_kernel, mV, mZ, mW, p);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace ttt
