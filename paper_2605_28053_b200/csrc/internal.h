@@ -1,6 +1,7 @@
 // Internal declarations shared by the host library (pool/planner/api) and
 // the sm_100a kernels.  Not part of the public ABI (that is include/tttstate.h).
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 
@@ -81,6 +82,7 @@ struct ChunkLaunch {
   const struct LowRankRead *lr = nullptr;   // non-null: fused low-rank READ (u = A x, finish) in this launch
   int *lr_ctr = nullptr;                    // fused mode counters [u_done, exit, tickets...], zero at rest
   int x_rowmap = 0;                         // X is [rows][d_ff] (2-D map, rows past n zero-filled)
+  int cooperative = 0;                      // fused mode: cooperative launch (several low-rank pools live)
 };
 
 // NEXT f1: low-rank delta READ / WRITE (DeltaAdapterState).
@@ -112,6 +114,7 @@ struct LowRankWrite {
   int owner_idx[kMaxGroup];
 };
 bool read_chunk_fused_fits(int row_blocks, int d_model, int ksplit);
+extern std::atomic<int> g_live_lowrank_pools;
 cudaError_t launch_lowrank_read(const LowRankRead &p, const ChunkLaunch &base, cudaStream_t s);
 cudaError_t launch_lowrank_write(const LowRankWrite &p, cudaStream_t s);
 

@@ -274,6 +274,7 @@ cudaError_t launch_lowrank_read(const LowRankRead &p0, const ChunkLaunch &base0,
     }
     base.lr = &p;
     base.lr_ctr = p.ctr;
+    base.cooperative = g_live_lowrank_pools.load() > 1;
     return launch_read_chunk(base, s);
   }
   p.nseg = lr_segments(p.n * p.rank, sms * (kUThreads / 32));

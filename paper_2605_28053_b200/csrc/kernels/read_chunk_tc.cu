@@ -68,6 +68,7 @@ struct ChunkParams {
   float *Y32;
   long long y32_slab;
   int x_rowmap;                  // X map is [rows][d_ff]: row block b starts at row 128·b
+  int cooperative;               // LR: launch cooperatively (co-residency guaranteed)
   int owner_idx[kMaxGroup];
   LrFused lr;
 };
@@ -449,11 +450,15 @@ cudaError_t launch_bn(const CUtensorMap &mX, const CUtensorMap &mW, const CUtens
   cfg.blockDim = dim3(LR ? kThreadsLR : kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  // the fused low-rank launch spin-waits across CTAs: a cooperative launch makes the driver
+  // guarantee that every CTA is co-resident (also against other streams' kernels)
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (LR && p.cooperative) ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, read_chunk_tc_kernel<BN, LR>, mX, mW, mD, p);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
@@ -552,6 +557,7 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
   p.ksplit = cl.ksplit < 1 ? 1 : cl.ksplit;
   p.y32_slab = cl.y32_slab;
   p.x_rowmap = cl.x_rowmap;
+  p.cooperative = cl.cooperative;
   for (int b = 0; b < cl.n; ++b) p.owner_idx[b] = cl.owner_idx[b];
   const int sms = device_sm_count();
   const NPlan np = plan_n(cl.d_model, cl.n * std::max(1, cl.ksplit), sms);

@@ -19,6 +19,10 @@ namespace ttt {
 static thread_local std::string g_last_error;
 static std::atomic<long long> g_launches{0};
 static std::atomic<int> g_write_impl{0};
+// Live device low-rank pools in this process: the fused low-rank READ spin-waits across its
+// CTAs, so with two such pools (two streams) its launches become cooperative (co-residency
+// guaranteed by the driver); a lone pool keeps the cheaper PDL launch.
+std::atomic<int> g_live_lowrank_pools{0};
 
 void count_launch(int n) { g_launches += n; }
 
@@ -234,11 +238,13 @@ ttt_status tttstate_pool_create(const ttt_shape *shape, int32_t shape_id, int32_
       return cuda_fail(e, "pool tables init");
     }
   }
+  if (!p->host_only && shape->backend == TTT_LOW_RANK) g_live_lowrank_pools.fetch_add(1);
   *out = p;
   return TTT_OK;
 }
 
 ttt_status tttstate_pool_destroy(ttt_pool *pool) {
+  if (pool && !pool->host_only && pool->sh.backend == TTT_LOW_RANK) g_live_lowrank_pools.fetch_sub(1);
   delete pool;
   return TTT_OK;
 }

@@ -44,3 +44,28 @@ def test_config4_lowrank_branches_parity(rank, streams, d_model, d_ff):
         for l in range(tr.n_layers):
             A, B = read_lowrank(eng, tr, b, l)
             assert nm.normwise_rel_err(A, S[l][0]) <= tol and nm.normwise_rel_err(B, S[l][1]) == 0.0
+
+
+def test_two_lowrank_pools_on_two_streams():
+    """Two low-rank pools driven concurrently on two CUDA streams (the fused READ spin-waits
+    across CTAs, so with two live pools it launches cooperatively): both match the oracle."""
+    trs = [T.config4_lowrank(n_steps=18, n_layers=2, rank=16, d_model=256, d_ff=384, chunk=8, n_streams=24,
+                             seed=40 + k).replace(B=24, owner_base=5000 * (k + 1)) for k in range(2)]
+    refs = [run_batched(tr) for tr in trs]
+    engs = [make_engine(tr, DEV, n_ckpt=26, max_owners=50) for tr in trs]
+    srcs = [HostGenInputs(tr, DEV) for tr in trs]
+    streams = [torch.cuda.Stream() for _ in trs]
+    from paper_2605_28053_b200.serving import Server
+    srvs = [Server(e, tr, src, stream=st) for e, tr, src, st in zip(engs, trs, srcs, streams)]
+    for srv in srvs:
+        srv.admit()
+    while not all(srv.done() for srv in srvs):                  # interleave the two serving loops
+        for srv in srvs:
+            if not srv.done():
+                srv.step()
+    torch.cuda.synchronize()
+    for srv, tr, ref, src in zip(srvs, trs, refs, srcs):
+        log = srv.finish()
+        assert log.versions == ref.versions and log.commits == ref.commits
+        worst = max(nm.normwise_rel_err(src.out[k], ref.outputs[k]) for k in ref.outputs)
+        assert worst <= nm.TOL["bf16"], worst
