@@ -196,3 +196,27 @@ def test_all_update_streaming_learner_controls(dtype, impl):
         capi.tttstate_set_write_impl(prev)
     _compare(tr, ref, src, log, eng)
     assert log.fallbacks == 2
+
+
+def _random_shapes(n, seed):
+    g = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        dtype = ["bf16", "bf16", "fp32"][g.integers(3)]
+        vec = 8 if dtype == "bf16" else 4
+        d_model = int(g.integers(4, 120)) * 4                       # multiples of 4, not of 16 / 128
+        d_ff = int(g.integers(2, 160)) * vec
+        streams = int(g.integers(1, 13))
+        chunk = int([1, 2, 3, 5, 16][g.integers(5)])
+        out.append((dtype, d_model, d_ff, streams, chunk, int(g.integers(1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("dtype,d_model,d_ff,streams,chunk,seed", _random_shapes(6, 2026))
+def test_random_shapes_parity(dtype, d_model, d_ff, streams, chunk, seed):
+    """Seeded random shapes: ragged row blocks / K chunks / vector tails, 1..12 members
+    (split READ launches), C = 1 (fused f3 path) to 16, both dtypes, two boundaries."""
+    tr = T.uniform_small(n_streams=streams, n_layers=2, d_model=d_model, d_ff=d_ff, chunk=chunk,
+                         n_steps=2 * chunk + 1, dtype=dtype, delta0="rng", v0=1, seed=seed % 1000)
+    ref, src, log, eng = _run(tr)
+    _compare(tr, ref, src, log, eng)
