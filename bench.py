@@ -301,6 +301,10 @@ def main():
     ms_max = D.max_over_ranks(ms, coll_dev)
     tokens_total = world * a.steps * window * N_STREAMS
     value = tokens_total / (ms_max / 1e3)
+    # end-of-run gather: every rank's owner versions (owners must be disjoint
+    # across ranks) and the census summed over ranks — metadata only, after the timed region
+    versions_all = D.gather_dict({o: capi.tttstate_version(eng.pool, o) for o in srv.owners})
+    census_all = {k: int(D.sum_over_ranks(v, coll_dev)) for k, v in sorted(census.items())}
 
     # ---- e2e: the same loop through the public API with every window's inputs copied H2D from
     # pinned host memory and its outputs D2H inside the timed region.  Two device buffer sets:
@@ -396,7 +400,8 @@ def main():
             "step_roofline": {"ms_per_step": roof_ms, "tok_s_per_gpu": roof_tok_s,
                               "frac": (value / world) / roof_tok_s,
                               "bytes_per_step": window * L * read_bytes + write_bytes},
-            "census": census,
+            "census": census_all,
+            "owners_all_ranks": {"n": len(versions_all), "versions": sorted(set(versions_all.values()))},
             "planner_host_share": plan_s / wall_s,
             "host_wall_ms_per_step": wall_s * 1e3 / a.steps,
             "clocks": clk.summary(),
