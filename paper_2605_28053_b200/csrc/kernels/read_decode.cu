@@ -327,6 +327,7 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint3
 }
 
 constexpr int kMmaThreads = 1024, kMmaChunkVec = 64;   // 512 bf16 of K per base task
+constexpr int kDU = 4;                                  // ΔW loads per lane per batch (= the preloaded batch)
 
 __host__ __device__ inline int mma_nvp(int nvec) { return (nvec + 127) / 128 * 128; }
 
@@ -496,64 +497,58 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
   }
   if (t >= n_tasks) return;
 
-  // ---- phase 2: ΔW rows (SIMT GEMVs, FHFMA), the next batch always in flight; the task's
-  // (member, row) are decoded once per task, not per batch
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  // ---- phase 2: ΔW rows (SIMT GEMVs, FHFMA). Plain batches: issue kDU 16-byte loads per
+  // lane, then consume them. Measured faster than the register double buffer with
+  // cross-task prefetch it replaced (76.7 vs 78.9 µs sustained, 0.90 vs 0.88 burst): with 32
+  // warps per SM the other warps already hide a batch's latency, and the simpler loop keeps
+  // registers (no spills) and instructions down.
   uint32_t expmax = 0;
-  int m = (t - n_base) / dm, i = (t - n_base) - m * dm;
-  while (true) {
-    int nv = v + 128, nt = t, nm = m, ni = i;
-    const uint4 *nrow = row;
-    const bool task_end = nv >= nvec;
-    if (task_end) {
-      nt = t + stride;
-      nv = lane;
-      if (nt < n_tasks) {
-        const int td = nt - n_base;
-        nm = td / dm;
-        ni = td - nm * dm;
-        nrow = s_row0[nm + 1] + (size_t)ni * nvec;
-      }
-    }
-    const bool more = nt < n_tasks;
-    if (more) load_delta(nxt, nrow, nv);
-    const uint4 *xb = xs + (size_t)m * nvp + v;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) E::dot(acc[u], cur[u], xb[32 * u]);
+  bool have_cur = true;                          // the first ΔW batch is preloaded (before x staging, or by the base phase)
+  for (; t < n_tasks; t += stride) {
+    const int td = t - n_base, m = td / dm, i = td - m * dm;
+    const uint4 *rw = s_row0[m + 1] + (size_t)i * nvec;
+    const uint4 *xb = xs + (size_t)m * nvp;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float ev = 0.f;
+    uint4 *drow = nullptr;
     if (FUSE) {
-      const float ev = p.eta * E::to_f(static_cast<const __nv_bfloat16 *>(p.Vt)[(size_t)p.v_row[m] * dm + i]);
-      uint4 *drow = s_dst0[m] + (size_t)i * nvec;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (v + 32 * u < nvec) drow[v + 32 * u] = Upd<__nv_bfloat16>::apply(cur[u], xb[32 * u], ev, expmax);
+      ev = p.eta * E::to_f(static_cast<const __nv_bfloat16 *>(p.Vt)[(size_t)p.v_row[m] * dm + i]);
+      drow = s_dst0[m] + (size_t)i * nvec;
     }
-    if (task_end) {
-      float sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    for (int v0 = lane; v0 < nvec; v0 += 32 * kDU) {
+      uint4 w[kDU];
+      if (have_cur) {                            // (kDU == 4: the preloaded batch is this one)
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-      if (lane == 0) p.Pdelta[(size_t)m * dm + i] = sum;
-      __syncwarp();
-      int old = 0;
-      if (lane == 0) {
-        __threadfence();
-        old = atomicAdd(p.tickets + i, 1);
-      }
-      old = __shfl_sync(0xffffffffu, old, 0);
-      if (old == target - 1) {
-        __threadfence();
-        combine(i);
+        for (int u = 0; u < kDU; ++u) w[u] = cur[u & 3];
+        have_cur = false;
+      } else {
+#pragma unroll
+        for (int u = 0; u < kDU; ++u)
+          w[u] = v0 + 32 * u < nvec ? ld_stream(rw + v0 + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = 0.f;
-    }
-    if (!more) break;
+      for (int u = 0; u < kDU; ++u) E::dot(acc[u & 3], w[u], xb[v0 + 32 * u]);
+      if (FUSE) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
-    v = nv;
-    row = nrow;
-    t = nt;
-    m = nm;
-    i = ni;
+        for (int u = 0; u < kDU; ++u)
+          if (v0 + 32 * u < nvec) drow[v0 + 32 * u] = Upd<__nv_bfloat16>::apply(w[u], xb[v0 + 32 * u], ev, expmax);
+      }
+    }
+    float sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    if (lane == 0) p.Pdelta[(size_t)m * dm + i] = sum;
+    __syncwarp();
+    int old = 0;
+    if (lane == 0) {
+      __threadfence();
+      old = atomicAdd(p.tickets + i, 1);
+    }
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old == target - 1) {
+      __threadfence();
+      combine(i);
+    }
   }
   if (FUSE && Upd<__nv_bfloat16>::bad(expmax)) atomicOr(p.fail_flag, 1);
 }
