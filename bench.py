@@ -366,6 +366,23 @@ def main():
         if os.path.exists(tf):
             traffic = json.load(open(tf)).get("read_decode_kernel", {}).get("dram_bytes_per_launch")
         write_bytes = N_STREAMS * (2 * D_MODEL * D_FF * 2 + CHUNK * (D_FF + D_MODEL) * 2) * L
+        # BJ metric's "READ TC%": tensor-pipe share from the committed ncu captures (never timed here)
+        tc = {}
+        for key, fn, metric in (("read_decode", "read_decode_ncu.txt",
+                                 "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                                ("read_chunk_8_members", "read_chunk_tc_ncu.txt",
+                                 "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed")):
+            path = os.path.join(ROOT, "profiles", "r1", fn)
+            if os.path.exists(path):
+                for line in open(path):
+                    if line.startswith(metric):
+                        tc[key] = float(line.split("=")[1].split()[0])
+        b64 = os.path.join(ROOT, "profiles", "r1", "read_chunk_b64_launches.csv")
+        if os.path.exists(b64):
+            vals = [float(r[-1]) for r in __import__("csv").reader(open(b64))
+                    if len(r) > 3 and "tensor" in r[-3]]
+            if vals:
+                tc["read_chunk_64_members"] = sum(vals) / len(vals)
         write_avg = sum(write_ms) / len(write_ms) if write_ms else None
         # whole-step roofline: every byte of the window's READs and its boundary WRITE at HBM peak
         roof_ms = (window * L * read_bytes + write_bytes) / (hbm * 1e9) * 1e3
@@ -397,6 +414,7 @@ def main():
                       "alg_bytes_per_call": write_bytes},
             # READ launches per timed window: L per decode step; events sample 1 step in 8
             "read_share_of_step": read_avg * L * window * a.steps / ms,
+            "read_tensor_pipe_pct_ncu": tc or None,
             "step_roofline": {"ms_per_step": roof_ms, "tok_s_per_gpu": roof_tok_s,
                               "frac": (value / world) / roof_tok_s,
                               "bytes_per_step": window * L * read_bytes + write_bytes},
