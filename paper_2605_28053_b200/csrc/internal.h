@@ -101,6 +101,8 @@ struct LowRankRead {
   void *tailZ, *tailV;
   long long tz_owner, tv_owner, tz_layer, tv_layer;
   int owner_idx[kMaxGroup], x_row[kMaxGroup], v_row[kMaxGroup], y_row[kMaxGroup], tail_pos[kMaxGroup];
+  const void *w_down = nullptr;  // [L][d_model][d_ff] (tensor maps of the one-pass kernel)
+  int L = 0, layer = 0, max_slots = 0;
 };
 struct LowRankWrite {
   int n, d_model, d_ff, rank, C;
@@ -117,6 +119,8 @@ bool read_chunk_fused_fits(int row_blocks, int d_model, int ksplit);
 extern std::atomic<int> g_live_lowrank_pools;
 cudaError_t launch_lowrank_read(const LowRankRead &p, const ChunkLaunch &base, cudaStream_t s);
 cudaError_t launch_lowrank_write(const LowRankWrite &p, cudaStream_t s);
+bool lowrank_tc_supported(int n, int d_model, int d_ff, int rank);
+cudaError_t launch_lowrank_tc(const LowRankRead &p, const void *X, cudaStream_t s);   // one-pass READ
 
 int device_sm_count();
 bool read_chunk_supported(int d_model, int d_ff, int C);

@@ -258,11 +258,23 @@ cudaError_t launch_lowrank_read(const LowRankRead &p0, const ChunkLaunch &base0,
   LowRankRead p = p0;
   ChunkLaunch base = base0;
   const int sms = device_sm_count();
-  static const bool fused_on = !getenv("TTT_LR_FUSED") || atoi(getenv("TTT_LR_FUSED")) != 0;
-  if (fused_on && read_chunk_fused_fits(base.n, p.d_model, base.ksplit)) {
+  // TTT_LR_FUSED: 1 (default) base GEMM + u warps + finish in one launch (read_chunk_tc.cu),
+  // 2 one-pass tcgen05 GEMM over [W_down; A] + bulk-copy finish (lowrank_tc.cu; measured equal
+  // at R = 64 and 8 % slower at R = 16), 0 three launches
+  static const int mode = getenv("TTT_LR_FUSED") ? atoi(getenv("TTT_LR_FUSED")) : 1;
+  bool identity = true;
+  for (int b = 0; b < p.n; ++b) identity &= p.x_row[b] == b;
+  if (mode == 2 && lowrank_tc_supported(p.n, p.d_model, p.d_ff, p.rank)) {
+    if (!identity) {
+      lr_gather_kernel<<<sms * 4, 256, 0, s>>>(p);
+      count_launch();
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    return launch_lowrank_tc(p, identity ? p.X : p.Xg, s);
+  }
+  if (mode != 0 && read_chunk_fused_fits(base.n, p.d_model, base.ksplit)) {
     // one launch: base GEMM on tcgen05 + u = A x warps + tail append + finish (read_chunk_tc.cu)
-    bool identity = true;
-    for (int b = 0; b < p.n; ++b) identity &= p.x_row[b] == b;
     if (identity) {
       base.X = p.X;
       base.x_rowmap = 1;

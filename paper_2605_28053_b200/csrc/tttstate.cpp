@@ -436,6 +436,10 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
     lp.ksplit = cl.ksplit;
     lp.y32_slab = cl.y32_slab;
     lp.ctr = reinterpret_cast<int *>(p->arena + p->lay.Ctr);
+    lp.w_down = p->w_down;
+    lp.L = sh.n_layers;
+    lp.layer = layer;
+    lp.max_slots = 2 * p->max_owners + p->n_ckpt;
     cudaError_t e = launch_lowrank_read(lp, cl, s);
     if (e != cudaSuccess) return cuda_fail(e, "low-rank READ");
     for (int b = 0; b < g->n; ++b) {
