@@ -38,6 +38,7 @@ struct ReadParams {
   int order;                     // task order: 0 CTA-major, 1 SM-interleaved (balanced bytes per SM)
   int dyn;                       // per-CTA dynamic task hand-out (SM-interleaved order only)
   int kc;                        // > 0: tensor-core base (bf16), Pbase holds kc K-chunk slabs [kc][8][d_model]
+  int l2keep;                    // not the group's last launch of this layer: keep W_down in L2 (evict_last)
 };
 
 // a5: chunk update of one layer for every member (shadow slot <- ΔW_v + η VᵀZ).

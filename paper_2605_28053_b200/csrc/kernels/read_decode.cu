@@ -47,6 +47,22 @@ __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
   return r;
 }
 
+// L2 eviction-priority variants (configs with several READ launches per layer: W_down[l] is kept
+// in L2 across the group's launches, the once-read ΔW rows are evicted first)
+__device__ __forceinline__ u64 l2_policy(bool last) {
+  u64 pol;
+  if (last) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ld_stream_hint(const uint4 *p, u64 pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
 // acc += w.lo*x.lo + w.hi*x.hi for one packed bf16 pair (fp32 accumulate)
 __device__ __forceinline__ void fma_bf16x2(float &acc, uint32_t w, uint32_t x) {
   asm("{\n\t.reg .b16 wl, wh, xl, xh;\n\t"
@@ -331,7 +347,7 @@ constexpr int kDU = 4;                                  // ΔW loads per lane pe
 
 __host__ __device__ inline int mma_nvp(int nvec) { return (nvec + 127) / 128 * 128; }
 
-template <bool FUSE>
+template <bool FUSE, bool L2H>
 __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const ReadParams p) {
   constexpr int kWarps = kMmaThreads / 32;
   using E = Elem<__nv_bfloat16>;
@@ -360,21 +376,24 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
   };
   if (tid == 0) s_next = kWarps;
   const uint4 *W = static_cast<const uint4 *>(p.w_down_l);
+  const u64 pol_w = L2H ? l2_policy(true) : 0ull, pol_d = L2H ? l2_policy(false) : 0ull;
+  auto ldw = [&](const uint4 *q) { return L2H ? ld_stream_hint(q, pol_w) : ld_stream(q); };
+  auto ldd = [&](const uint4 *q) { return L2H ? ld_stream_hint(q, pol_d) : ld_stream(q); };
 
   // base task tt: rows r0 = 16·(tt / KC) (+g, +g+8) × vectors {8j + tq, 8j + 4 + tq} of K chunk tt % KC
   auto load_base = [&](uint4 (&buf)[4], int tt, int j) {
     const int rb = tt / KC, kc = tt - rb * KC, r = rb * 16 + g, v0 = kc * kMmaChunkVec + 8 * j + tq;
     const uint4 *q = W + (size_t)r * nvec + v0;
     const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-    buf[0] = (r < dm && v0 < nvec) ? ld_stream(q) : z;
-    buf[1] = (r < dm && v0 + 4 < nvec) ? ld_stream(q + 4) : z;
-    buf[2] = (r + 8 < dm && v0 < nvec) ? ld_stream(q + 8 * (size_t)nvec) : z;
-    buf[3] = (r + 8 < dm && v0 + 4 < nvec) ? ld_stream(q + 8 * (size_t)nvec + 4) : z;
+    buf[0] = (r < dm && v0 < nvec) ? ldw(q) : z;
+    buf[1] = (r < dm && v0 + 4 < nvec) ? ldw(q + 4) : z;
+    buf[2] = (r + 8 < dm && v0 < nvec) ? ldw(q + 8 * (size_t)nvec) : z;
+    buf[3] = (r + 8 < dm && v0 + 4 < nvec) ? ldw(q + 8 * (size_t)nvec + 4) : z;
   };
   // ΔW task: 4 × 32 lanes of one row
   auto load_delta = [&](uint4 (&buf)[4], const uint4 *rw, int v0) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) buf[u] = v0 + 32 * u < nvec ? ld_stream(rw + v0 + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
+    for (int u = 0; u < 4; ++u) buf[u] = v0 + 32 * u < nvec ? ldd(rw + v0 + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
   };
 
   uint4 cur[4], nxt[4];
@@ -524,7 +543,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
       } else {
 #pragma unroll
         for (int u = 0; u < kDU; ++u)
-          w[u] = v0 + 32 * u < nvec ? ld_stream(rw + v0 + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
+          w[u] = v0 + 32 * u < nvec ? ldd(rw + v0 + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll
       for (int u = 0; u < kDU; ++u) E::dot(acc[u & 3], w[u], xb[v0 + 32 * u]);
@@ -619,12 +638,12 @@ bool read_decode_fits(int n, int d_model, int d_ff, int esize) {
 }
 
 namespace {
-template <bool FUSE>
+template <bool FUSE, bool L2H>
 cudaError_t launch_mma(const ReadParams &p, cudaStream_t s) {
   const size_t smem = (size_t)kMaxReadMembers * mma_nvp(p.d_ff / 8) * 16;
   static size_t configured = 0;
   if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(read_decode_mma_kernel<FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(read_decode_mma_kernel<FUSE, L2H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return e;
     configured = smem;
@@ -645,7 +664,7 @@ cudaError_t launch_mma(const ReadParams &p, cudaStream_t s) {
   ReadParams q = p;
   q.order = order;
   q.dyn = order == 1 ? dyn : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, read_decode_mma_kernel<FUSE>, q);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, read_decode_mma_kernel<FUSE, L2H>, q);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -660,7 +679,17 @@ int read_decode_mma_chunks(int dtype, int d_ff) {
 }
 
 cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s) {
-  if (p.kc > 0) return p.fuse ? launch_mma<true>(p, s) : launch_mma<false>(p, s);
+  static const int l2keep = getenv("TTT_READ_L2KEEP") ? atoi(getenv("TTT_READ_L2KEEP")) : 1;
+  static const int persist_mb = getenv("TTT_L2_PERSIST_MB") ? atoi(getenv("TTT_L2_PERSIST_MB")) : 0;
+  static bool limit_set = false;
+  if (persist_mb > 0 && !limit_set) {
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist_mb << 20);
+    limit_set = true;
+  }
+  if (p.kc > 0) {
+    if (p.l2keep && l2keep) return p.fuse ? launch_mma<true, true>(p, s) : launch_mma<false, true>(p, s);
+    return p.fuse ? launch_mma<true, false>(p, s) : launch_mma<false, false>(p, s);
+  }
   if (dtype == 1) return launch_t<__nv_bfloat16>(p, s);
   return launch_t<float>(p, s);
 }

@@ -472,6 +472,7 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
     rp.Pdelta = rp.Pbase + (size_t)std::max(1, rp.kc) * kMaxReadMembers * sh.d_model;
     rp.tickets = reinterpret_cast<int *>(p->arena + p->lay.tickets);
     rp.n = std::min(per, g->n - b0);
+    rp.l2keep = g->n > per;                        // several launches read this layer's W_down
     rp.d_model = sh.d_model; rp.d_ff = sh.d_ff;
     rp.fuse = fuse ? 1 : 0;
     rp.eta = p->eta;
