@@ -257,6 +257,13 @@ def main():
             rows = self._rows
             return self.X[l], rows, self.V[l], rows, self.Y[l], rows
 
+    # start of run: rank 0's config and owner→rank map to every rank; each
+    # rank checks that the owners it serves are exactly the ones the map places on it
+    run_cfg = D.broadcast_config({"n_streams_per_rank": N_STREAMS, "layers": L, "chunk": CHUNK,
+                                  "placement": {1000 + 100 * r + s: r for r in range(world)
+                                                for s in range(N_STREAMS)}} if rank == 0 else None)
+    assert sorted(o for o, r in run_cfg["placement"].items() if r == rank) == \
+        [tr.owner(s) for s in range(N_STREAMS)], "owner map disagrees with this rank's owners"
     src = Window()
     stream = torch.cuda.current_stream(dev)
     srv = Server(eng, tr, src, stream=stream, sync_writes=True, profile=True, profile_every=8)
@@ -264,9 +271,14 @@ def main():
     torch.cuda.synchronize(dev)
     del src.d0
 
+    stats = D.StatsExchange(3, coll_dev)
+
     def run_window():
+        c0 = dict(srv.log.census)
         for _ in range(window):
             srv.step()
+        # per-step metadata exchange: this window's census, async on a side stream
+        stats.post([srv.log.census.get(0, 0) - c0.get(0, 0), srv.log.census.get(1, 0) - c0.get(1, 0), window])
 
     def barrier():
         if world > 1:
@@ -305,6 +317,8 @@ def main():
     # across ranks) and the census summed over ranks — metadata only, after the timed region
     versions_all = D.gather_dict({o: capi.tttstate_version(eng.pool, o) for o in srv.owners})
     census_all = {k: int(D.sum_over_ranks(v, coll_dev)) for k, v in sorted(census.items())}
+    ex_tot = stats.totals().sum(0).tolist()          # every window so far (warm-up + timed), all ranks
+    assert ex_tot[0] >= census_all.get("READ", 0) and ex_tot[1] >= census_all.get("WRITE", 0), (ex_tot, census_all)
 
     # ---- e2e: the same loop through the public API with every window's inputs copied H2D from
     # pinned host memory and its outputs D2H inside the timed region.  Two device buffer sets:
@@ -419,6 +433,8 @@ def main():
                               "frac": (value / world) / roof_tok_s,
                               "bytes_per_step": window * L * read_bytes + write_bytes},
             "census": census_all,
+            "stats_exchange": {"READ": ex_tot[0], "WRITE": ex_tot[1], "decode_steps": ex_tot[2],
+                               "note": "per-window async all_gather on a side stream, warm-up + timed windows"},
             "owners_all_ranks": {"n": len(versions_all), "versions": sorted(set(versions_all.values()))},
             "planner_host_share": plan_s / wall_s,
             "host_wall_ms_per_step": wall_s * 1e3 / a.steps,

@@ -107,3 +107,37 @@ def _collide(rank, world, port):
         raise SystemExit(3)
     finally:
         dist.destroy_process_group()
+
+
+def _exchange_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = {"streams": 13, "placement": {D.owner_id(s): s % world for s in range(13)}} if rank == 0 else None
+        cfg = D.broadcast_config(cfg)
+        mine = [o for o, r in cfg["placement"].items() if r == rank]
+        assert mine == [D.owner_id(s) for s in D.shard_streams(cfg["streams"], world, rank)]
+        ex = D.StatsExchange(3)
+        for step in range(5):                                   # per-step async exchange
+            ex.post([len(mine), rank, step])
+        tot = ex.totals()
+        if rank == 0:
+            q.put(tot.tolist())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_config_broadcast_and_async_stats_exchange():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    tot = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # rank 0 owns streams 0,2,..,12 (7), rank 1 owns 6; 5 steps; step ids sum to 10
+    assert tot == [[35, 0, 10], [30, 5, 10]]
