@@ -21,6 +21,8 @@
 
 #include "pool.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 struct ttt_planner {
   int mode = TTT_MODE_FULL, B = 8, w = 0;
   std::vector<ttt_pool *> pools;
@@ -90,6 +92,10 @@ ttt_status ttt_planner_pending(ttt_planner *pl, int32_t *n_out) {
 ttt_status plan_batch(ttt_planner *pl, const ttt_event *events, int32_t n, int64_t clock, ttt_group *out,
                       int32_t cap, uint64_t *owner_buf, int32_t owner_cap, int32_t *n_out, ttt_event *rejected,
                       int32_t rej_cap, int32_t *n_rej) {
+  nvtxRangePushA("plan_batch");
+  struct Pop {
+    ~Pop() { nvtxRangePop(); }
+  } pop_;
   if (!pl || (n > 0 && !events) || !n_out || !n_rej || n < 0) return perr(TTT_E_INVALID_ARG, "null arg");
   auto buckets = pl->buckets;                        // work on a copy: no side effect on error
   std::vector<ttt_event> rej;

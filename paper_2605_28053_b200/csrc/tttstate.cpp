@@ -14,6 +14,17 @@
 
 #include "pool.h"
 
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX ranges around the hot-path entry points (SURVEY §5 tracing): no-ops unless a tool
+// (Nsight Systems / ncu --nvtx) is attached; `ncu --nvtx --nvtx-include "read_apply/"` filters
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 namespace ttt {
 
 static thread_local std::string g_last_error;
@@ -369,6 +380,7 @@ ttt_status validate_group(ttt_pool *p, const ttt_group *g, const uint64_t *expec
 ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void *X, const int32_t *x_rows,
                       const void *Vt, const int32_t *v_rows, void *Y, const int32_t *y_rows,
                       const void *resid, void *stream) {
+  NvtxRange nvtx_("read_apply");
   std::vector<OwnerRec *> recs;
   ttt_status st = check_group(p, g, recs);
   if (st != TTT_OK) return st;
@@ -519,6 +531,7 @@ ttt_status tttstate_step_done(ttt_pool *p, const ttt_group *g) {
 
 ttt_status read_apply_chunk(ttt_pool *p, const ttt_group *g, int32_t layer, const void *X, const void *Vt,
                             void *Y, void *stream) {
+  NvtxRange nvtx_("read_apply_chunk");
   std::vector<OwnerRec *> recs;
   ttt_status st = check_group(p, g, recs);
   if (st != TTT_OK) return st;
@@ -563,6 +576,7 @@ ttt_status read_apply_chunk(ttt_pool *p, const ttt_group *g, int32_t layer, cons
 // ---------------------------------------------------------------- WRITE + commit
 ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32_t *fail_mask,
                         uint64_t *new_versions, void *stream) {
+  NvtxRange nvtx_("write_commit");
   std::vector<OwnerRec *> recs;
   ttt_status st = check_group(p, g, recs);
   if (st != TTT_OK) return st;
@@ -654,6 +668,7 @@ ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32
 
 // ---------------------------------------------------------------- control
 ttt_status tttstate_snapshot(ttt_pool *p, uint64_t owner, void *stream) {
+  NvtxRange nvtx_("tttstate_snapshot");
   (void)stream;
   if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
   OwnerRec *r;
@@ -668,6 +683,7 @@ ttt_status tttstate_snapshot(ttt_pool *p, uint64_t owner, void *stream) {
 }
 
 ttt_status rollback(ttt_pool *p, uint64_t owner, uint64_t *v_out, void *stream) {
+  NvtxRange nvtx_("rollback");
   if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
   OwnerRec *r;
   ttt_status st = find_owner(p, owner, &r);
@@ -693,6 +709,7 @@ ttt_status rollback(ttt_pool *p, uint64_t owner, uint64_t *v_out, void *stream) 
 }
 
 ttt_status tttstate_fork(ttt_pool *p, uint64_t src, uint64_t dst, void *stream) {
+  NvtxRange nvtx_("tttstate_fork");
   if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
   OwnerRec *rs;
   ttt_status st = find_owner(p, src, &rs);
@@ -714,6 +731,7 @@ ttt_status tttstate_fork(ttt_pool *p, uint64_t src, uint64_t dst, void *stream) 
 }
 
 ttt_status tttstate_sync(ttt_pool *p, void *stream, int32_t *n_failed_out) {
+  NvtxRange nvtx_("tttstate_sync");
   if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
   if (n_failed_out) *n_failed_out = 0;
   if (p->host_only) return TTT_OK;
