@@ -156,6 +156,24 @@ class OracleSample:
                 "window_s": window_s}
 
 
+def sampled_parity(samples):
+    """Oracle READ (fp64, y = (W_down + ΔW_v)·z, oracle/numerics.apply_read) on bench outputs
+    sampled from the last timed window, in the launch configuration bench.py times; the
+    normwise error (reading xii) against BASELINE.json's bf16 tolerance."""
+    from oracle import numerics as nm
+
+    worst, n = 0.0, 0
+    for _o, _l, w, d, x, y in samples:
+        W64, D64 = nm.widen(w, "bf16"), nm.widen(d, "bf16")
+        for k in range(x.shape[0]):
+            ref = nm.apply_read(W64, D64, nm.widen(x[k], "bf16"))
+            worst = max(worst, nm.normwise_rel_err(nm.widen(y[k], "bf16"), ref))
+            n += 1
+    return {"samples": n, "max_normwise_err": worst, "tol": nm.TOL["bf16"], "ok": bool(n and worst <= nm.TOL["bf16"]),
+            "what": "oracle READ on outputs of the last timed window: owners {first,last} x layers {0,L-1} x "
+                    "positions {0,64,127}, at the dW version those READs used"}
+
+
 def run_reference(a, rank, world):
     if rank != 0:
         return
@@ -188,6 +206,7 @@ def main():
     if a.impl == "reference":
         return run_reference(a, rank, world)
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -293,6 +312,7 @@ def main():
     torch.cuda.synchronize(dev)
     n_launch0 = capi.tttstate_launch_count()
     plan0, census0 = srv.plan_s, dict(srv.log.census)
+    nplan0 = len(srv.log.plan)
     wall0 = time.perf_counter()
     with ClockSampler(local) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -305,6 +325,12 @@ def main():
     wall_s = time.perf_counter() - wall0
     plan_s = srv.plan_s - plan0
     census = {("READ" if k == 0 else "WRITE"): v - census0.get(k, 0) for k, v in srv.log.census.items()}
+    # group-size and wait (issue − ready, Eq. 4) histograms of the timed region's plan log
+    size_hist, wait_hist = {}, {}
+    for issue, _eff, ss, ready in srv.log.plan[nplan0:]:
+        size_hist[len(ss)] = size_hist.get(len(ss), 0) + 1
+        for r_ in ready:
+            wait_hist[issue - r_] = wait_hist.get(issue - r_, 0) + 1
     barrier()
     ms = e0.elapsed_time(e1)
     read_spans = [(x.elapsed_time(y), n) for x, y, n in srv.read_events]
@@ -319,6 +345,23 @@ def main():
     census_all = {k: int(D.sum_over_ranks(v, coll_dev)) for k, v in sorted(census.items())}
     ex_tot = stats.totals().sum(0).tolist()          # every window so far (warm-up + timed), all ranks
     assert ex_tot[0] >= census_all.get("READ", 0) and ex_tot[1] >= census_all.get("WRITE", 0), (ex_tot, census_all)
+
+    # ---- sampled parity (checked in the cpu_baseline leg): the last timed window's outputs for
+    # owners {first, last} × layers {0, L-1} × positions {0, 64, 127} (127 = the WRITE step), with
+    # their inputs and the ΔW version those READs used — the slot the window's commit just retired
+    par_samples = []
+    if world == 1 and not a.no_cpu_baseline:
+        torch.cuda.synchronize(dev)
+        for s_ in (0, N_STREAMS - 1):
+            o_ = tr.owner(s_)
+            for l_ in sorted({0, L - 1}):
+                act = capi.tttstate_read_slot_raw(eng.pool, o_, -1, l_, D_MODEL, D_FF, "bf16", stream)
+                old = [capi.tttstate_read_slot_raw(eng.pool, o_, w_, l_, D_MODEL, D_FF, "bf16", stream) for w_ in (0, 1)]
+                prev = old[1] if np.array_equal(old[0], act) else old[0]
+                rows_ = [(p_ % CHUNK) * N_STREAMS + s_ for p_ in (0, 64, CHUNK - 1)]
+                par_samples.append((o_, l_, W[l_].view(torch.int16).cpu().numpy().view(np.uint16), prev,
+                                    src.X[l_][rows_].view(torch.int16).cpu().numpy().view(np.uint16),
+                                    src.Y[l_][rows_].view(torch.int16).cpu().numpy().view(np.uint16)))
 
     # ---- e2e: the same loop through the public API with every window's inputs copied H2D from
     # pinned host memory and its outputs D2H inside the timed region.  Two device buffer sets:
@@ -433,6 +476,9 @@ def main():
                               "frac": (value / world) / roof_tok_s,
                               "bytes_per_step": window * L * read_bytes + write_bytes},
             "census": census_all,
+            "groups": {"size_hist": {str(k): v for k, v in sorted(size_hist.items())},
+                       "wait_hist": {str(k): v for k, v in sorted(wait_hist.items())}},
+            "gpu": torch.cuda.get_device_name(dev),
             "stats_exchange": {"READ": ex_tot[0], "WRITE": ex_tot[1], "decode_steps": ex_tot[2],
                                "note": "per-window async all_gather on a side stream, warm-up + timed windows"},
             "owners_all_ranks": {"n": len(versions_all), "versions": sorted(set(versions_all.values()))},
@@ -444,6 +490,7 @@ def main():
             cb = OracleSample(1)()
             cb.pop("window_s", None)
             out["cpu_baseline"] = cb
+            out["parity"] = sampled_parity(par_samples)
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
