@@ -29,6 +29,8 @@ run(T.uniform_small(n_streams=3, n_layers=1, d_model=256, d_ff=256, chunk=16, n_
                     delta0="rng", controls={(0, 5): ["snapshot"], (0, 17): ["rollback"], (1, 15): ["fail"]}), impl=2)
 run(T.uniform_small(n_streams=3, n_layers=1, d_model=64, d_ff=128, chunk=1, n_steps=4, dtype="bf16", delta0="rng"))
 run(T.config4_lowrank(n_steps=10, n_layers=1, rank=4, d_model=256, d_ff=256, chunk=4, n_streams=3, seed=1))
+# rank 16 (a multiple of 8: the one-pass tcgen05 low-rank READ runs under TTT_LR_FUSED=2)
+run(T.config4_lowrank(n_steps=10, n_layers=1, rank=16, d_model=256, d_ff=256, chunk=4, n_streams=3, seed=2))
 # chunk READ
 tr = T.uniform_small(n_streams=2, n_layers=1, d_model=256, d_ff=256, chunk=16, n_steps=0, dtype="bf16")
 eng = make_engine(tr, "cuda")
