@@ -2,7 +2,9 @@
 parity suites in a subprocess: the all-SIMT bf16 decode READ (used when the tensor-core-base
 kernel's shared-memory staging does not fit, e.g. d_ff > 14,080), the three-launch low-rank
 READ (used when a fused launch would not fit one CTA per tile), the one-pass tcgen05 low-rank
-READ over [W_down; A] with its bulk-copy finish (TTT_LR_FUSED=2), and the serial-order READ."""
+READ over [W_down; A] with its bulk-copy finish (TTT_LR_FUSED=2), multi-launch READ groups
+with plain loads instead of the L2 evict_last / evict_first hints (TTT_READ_L2KEEP=0), and the
+serial-order READ."""
 import os
 import subprocess
 import sys
@@ -26,6 +28,7 @@ def _run(env_extra, target):
     ({"TTT_READ_MMA": "0", "TTT_READ_ORDER": "0"}, "tests/test_gpu_paper_dims.py"),
     ({"TTT_LR_FUSED": "0"}, "tests/test_gpu_lowrank.py"),
     ({"TTT_LR_FUSED": "2"}, "tests/test_gpu_lowrank.py"),
+    ({"TTT_READ_L2KEEP": "0"}, "tests/test_gpu_configs.py"),
 ])
 def test_alternative_paths_parity(env, target):
     _run(env, target)
