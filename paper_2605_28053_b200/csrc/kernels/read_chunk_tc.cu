@@ -499,8 +499,10 @@ NPlan plan_n(int d_model, int tiles_per_block_unit, int sms) {
     const long long tiles = (long long)T * tiles_per_block_unit;
     const long long waves = (tiles + sms - 1) / sms;
     const double cost = (double)waves * (128 + 2 * w_hi);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
+    // equal cost: prefer more blocks while they still fit one wave (more SMs streaming)
+    const bool more = cost < best_cost + 1e-9 && T > best.T && tiles <= sms;
+    if (cost < best_cost - 1e-9 || more) {
+      best_cost = std::min(best_cost, cost);
       best = {T, w_hi, h};
     }
   }
