@@ -43,7 +43,14 @@ constexpr int kEpiThreads = 256;                 // 8 epilogue warps: 2 per TMEM
 constexpr int kThreads = 64 + kEpiThreads;      // producer warp, MMA warp, 8 epilogue warps
 constexpr int kTmemCols = 2 * BN;                 // two fp32 accumulators of 128 columns
 constexpr int kBox = BM * 128;                    // one 128-row x 64-column bf16 box (16 KB)
-constexpr int kSB = 7;                            // committed-ΔW box ring depth (3.5 tiles ahead)
+#ifndef TTT_WRITE_SB
+#define TTT_WRITE_SB 7
+#endif
+#ifndef TTT_WRITE_ST
+#define TTT_WRITE_ST 3
+#endif
+constexpr int kSB = TTT_WRITE_SB;                 // committed-ΔW box ring depth (3.5 tiles ahead)
+constexpr int kST = TTT_WRITE_ST;                 // TMA stores in flight (read side); kSB - kST boxes of load lookahead
 
 typedef unsigned long long u64;
 
@@ -329,8 +336,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (et == 0) {
           tma_store_3d(&tmW, sS + sb * kBox, tl.jb * BN + 64 * h, tl.ib * BM, dst_slot * p.L + p.layer);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");   // box kb-2 has been read out
-          if (kb >= 2) mbar_arrive(s_empty + (kb - 2) % kSB);
+          asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kST) : "memory");   // box kb-kST read out
+          if (kb >= kST) mbar_arrive(s_empty + (kb - kST) % kSB);
         }
       }
     }
