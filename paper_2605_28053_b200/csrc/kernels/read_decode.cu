@@ -621,6 +621,9 @@ int read_cfg() {
 
 template <typename T>
 cudaError_t launch_t(const ReadParams &p, cudaStream_t s) {
+  // the fused C = 1 READ + WRITE (f3) streams two row sets per task (read + candidate store):
+  // 3 loads per lane per batch measured best for it (87 % vs 85 % of HBM with 4)
+  if (read_cfg() == 0 && p.fuse) return launch_cfg<T, 1024, 3>(p, s);
   switch (read_cfg()) {
     case 1: return launch_cfg<T, 1024, 3>(p, s);
     case 2: return launch_cfg<T, 1024, 2>(p, s);
