@@ -444,6 +444,7 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
     // 128 members, d 2560 / 9728)
     const int ntile = cl.n * ((sh.d_model + 159) / 160);
     cl.ksplit = std::max(1, std::min({kMaxKSplit, 2 * device_sm_count() / (3 * ntile), sh.d_ff / 64}));
+    if (const char *e = getenv("TTT_LR_KS")) cl.ksplit = std::max(1, std::min({kMaxKSplit, atoi(e), sh.d_ff / 64}));
     cl.y32_slab = (long long)align_up((size_t)p->max_owners, 128) * sh.d_model;
     lp.ksplit = cl.ksplit;
     lp.y32_slab = cl.y32_slab;
