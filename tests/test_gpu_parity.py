@@ -62,11 +62,13 @@ def test_config1_tiny_fp32_parity():
 
 
 @pytest.mark.parametrize("dtype,streams,d_model,d_ff", [("bf16", 9, 196, 328), ("fp32", 9, 196, 328),
-                                                      ("bf16", 3, 100, 1000), ("bf16", 8, 2560, 1224)])
+                                                      ("bf16", 3, 100, 1000), ("bf16", 8, 2560, 1224),
+                                                      ("bf16", 9, 200, 1536), ("bf16", 5, 64, 512)])
 def test_uniform_parity_ragged_and_split_groups(dtype, streams, d_model, d_ff):
     # 9 members > 8 per READ launch (split), d_model/d_ff not tile multiples, 2 boundaries;
     # bf16 decode runs the mma.sync base: ragged 16-row blocks (196, 100), ragged 512-wide K
-    # chunks (328, 1000, 1224), absent members (3 < 8), paper d_model (2560)
+    # chunks (328, 1000, 1224), absent members (3 < 8), paper d_model (2560); whole 512-wide
+    # K chunks only (1536: three, 512: one)
     tr = T.uniform_small(n_streams=streams, n_layers=2, d_model=d_model, d_ff=d_ff, chunk=8, n_steps=20,
                          dtype=dtype, delta0="rng", v0=5, seed=3)
     ref, src, log, eng = _run(tr)
