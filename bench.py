@@ -487,8 +487,15 @@ def main():
             "clocks": clk.summary(),
         }
         if world == 1 and not a.no_cpu_baseline:
-            cb = OracleSample(1)()
+            from threadpoolctl import threadpool_limits
+
+            sampler = OracleSample(1)
+            cb = sampler()
             cb.pop("window_s", None)
+            with threadpool_limits(limits=1):           # the 1-thread row beside it
+                c1 = sampler()
+            cb["one_thread"] = {"value": c1["value"], "unit": c1["unit"], "cores": 1,
+                                "sample": "the same sample with BLAS limited to 1 thread (threadpoolctl)"}
             out["cpu_baseline"] = cb
             out["parity"] = sampled_parity(par_samples)
         print(json.dumps(out), flush=True)
