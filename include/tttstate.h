@@ -241,6 +241,15 @@ int64_t tttstate_launch_count(void);
 /* Select the WRITE kernel: 0 = auto (tcgen05 for bf16 when available),
  * 1 = SIMT fp32-FFMA kernel, 2 = tcgen05 kernel.  Returns previous value.   */
 int32_t tttstate_set_write_impl(int32_t impl);
+/* Test hook for the stress suite's negative control ("disable
+ * rollback (test hook) -> MidGroupWriteFail scenario fails").  flags =
+ * TTT_HOOK_NO_GROUP_ATOMICITY breaks the group-atomic commit of write_commit
+ * (P:418-423): when an injected fail bit is set, the members whose bit
+ * is clear are published anyway (a non-atomic selective commit) and the call
+ * still returns TTT_E_WRITE_FAILED.  Process-wide; 0 restores the contract.
+ * Never set outside tests.  Returns the previous flags.                     */
+#define TTT_HOOK_NO_GROUP_ATOMICITY 1
+int32_t tttstate_set_test_hook(int32_t flags);
 
 #ifdef __cplusplus
 }

@@ -101,6 +101,7 @@ _sigs = {
     "tttstate_device_version": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_uint64), P]),
     "tttstate_launch_count": (C.c_int64, []),
     "tttstate_set_write_impl": (C.c_int32, [C.c_int32]),
+    "tttstate_set_test_hook": (C.c_int32, [C.c_int32]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(_lib, _name)
@@ -375,6 +376,14 @@ def tttstate_device_version(pool, owner: int, stream=None) -> int:
 
 def tttstate_launch_count() -> int:
     return _lib.tttstate_launch_count()
+
+
+TTT_HOOK_NO_GROUP_ATOMICITY = 1
+
+
+def tttstate_set_test_hook(flags: int) -> int:
+    """Stress-suite negative control only (include/tttstate.h); returns the previous flags."""
+    return _lib.tttstate_set_test_hook(flags)
 
 
 def tttstate_set_write_impl(impl: int) -> int:

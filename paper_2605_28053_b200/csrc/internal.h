@@ -64,6 +64,8 @@ struct CommitParams {
   int forced_fail;     // injected failure (host-known)
   int n;
   int owner_idx[kMaxGroup];
+  int partial;         // test hook (TTT_HOOK_NO_GROUP_ATOMICITY): publish members with no fail bit
+  unsigned fail_bits[kMaxGroup / 32];
 };
 
 // NEXT f2: chunk-granular READ of C tokens per member at one version (tcgen05).

@@ -21,8 +21,9 @@ __global__ void commit_kernel(const CommitParams p) {
   __shared__ int fail;
   if (threadIdx.x == 0) fail = p.forced_fail | *reinterpret_cast<volatile int *>(p.fail_flag);
   __syncthreads();
-  if (!fail) {
+  if (!fail || p.partial) {                      // p.partial: test hook only (negative control)
     for (int b = threadIdx.x; b < p.n; b += blockDim.x) {
+      if (fail && ((p.fail_bits[b / 32] >> (b % 32)) & 1u)) continue;
       const int o = p.owner_idx[b];
       p.sel[o] ^= 1;
       p.version[o] += 1ull;

@@ -30,6 +30,7 @@ namespace ttt {
 static thread_local std::string g_last_error;
 static std::atomic<long long> g_launches{0};
 static std::atomic<int> g_write_impl{0};
+static std::atomic<int> g_test_hook{0};   // tttstate_set_test_hook (stress negative control)
 // Live device low-rank pools in this process: the fused low-rank READ spin-waits across its
 // CTAs, so with two such pools (two streams) its launches become cooperative (co-residency
 // guaranteed by the driver); a lone pool keeps the cheaper PDL launch.
@@ -200,6 +201,7 @@ const char *tttstate_status_name(ttt_status s) {
 int64_t tttstate_launch_count(void) { return g_launches.load(); }
 
 int32_t tttstate_set_write_impl(int32_t impl) { return g_write_impl.exchange(impl); }
+int32_t tttstate_set_test_hook(int32_t flags) { return g_test_hook.exchange(flags); }
 
 // ---------------------------------------------------------------- pool
 ttt_status tttstate_pool_bytes(const ttt_shape *shape, int32_t max_owners, int32_t n_ckpt, size_t *bytes_out) {
@@ -654,7 +656,20 @@ ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32
   cp.forced_fail = forced ? 1 : 0;
   cp.n = g->n;
   for (int b = 0; b < g->n; ++b) cp.owner_idx[b] = recs[b]->idx;
+  const bool partial = forced && (g_test_hook.load() & TTT_HOOK_NO_GROUP_ATOMICITY);
+  cp.partial = partial ? 1 : 0;
+  if (partial)
+    for (int b = 0; b < g->n; ++b) cp.fail_bits[b / 32] = fail_mask[b / 32];
   CUDA_TRY(launch_commit(cp, s));
+  if (partial)                                    // the broken contract the negative control needs
+    for (int b = 0; b < g->n; ++b) {
+      if ((fail_mask[b / 32] >> (b % 32)) & 1u) continue;
+      OwnerRec &r = *recs[b];
+      r.sel ^= 1;
+      r.version += 1;
+      r.tail_len = 0;
+      clear_applied(r);
+    }
   if (forced) return fail(TTT_E_WRITE_FAILED, "injected failure: group not committed");
   for (int b = 0; b < g->n; ++b) {
     OwnerRec &r = *recs[b];
