@@ -363,6 +363,13 @@ def main():
                                     src.X[l_][rows_].view(torch.int16).cpu().numpy().view(np.uint16),
                                     src.Y[l_][rows_].view(torch.int16).cpu().numpy().view(np.uint16)))
 
+    # output digest of the last timed window (every layer's bf16 Y, all streams x C positions):
+    # the reductions run in a fixed order, so a rerun of the same command reproduces it exactly
+    import hashlib
+    torch.cuda.synchronize(dev)
+    out_digest = hashlib.sha256(src.Y.contiguous().view(torch.uint8).cpu().numpy().tobytes()).hexdigest()
+    digests = {str(k): v for k, v in sorted(D.gather_dict({rank: out_digest}).items())}
+
     # ---- e2e: the same loop through the public API with every window's inputs copied H2D from
     # pinned host memory and its outputs D2H inside the timed region.  Two device buffer sets:
     # window k+1's inputs and window k-1's outputs move on a copy stream while window k computes.
@@ -485,6 +492,9 @@ def main():
             "planner_host_share": plan_s / wall_s,
             "host_wall_ms_per_step": wall_s * 1e3 / a.steps,
             "clocks": clk.summary(),
+            "output_digest": {"sha256_by_rank": digests,
+                              "what": "bf16 Y of every layer for the last timed window (all streams x C "
+                                      "positions); fixed-order reductions: identical on reruns"},
         }
         if world == 1 and not a.no_cpu_baseline:
             from threadpoolctl import threadpool_limits
