@@ -222,3 +222,23 @@ def test_random_shapes_parity(dtype, d_model, d_ff, streams, chunk, seed):
                          n_steps=2 * chunk + 1, dtype=dtype, delta0="rng", v0=1, seed=seed % 1000)
     ref, src, log, eng = _run(tr)
     _compare(tr, ref, src, log, eng)
+
+
+def test_determinism_bitwise_rerun():
+    # SPEC acceptance criterion 10 (determinism): every reduction runs in a fixed order (per-row
+    # tickets, fixed-order partial sums, no data atomics), so rerunning a trace on fresh pools
+    # reproduces every READ output and every committed fast-weight byte exactly
+    tr = T.uniform_small(n_streams=8, n_layers=2, d_model=256, d_ff=1536, chunk=8, n_steps=17, dtype="bf16",
+                         delta0="rng", v0=3, seed=12)
+    runs = []
+    for _ in range(2):
+        eng = make_engine(tr, DEV)
+        src = HostGenInputs(tr, DEV)
+        log = run_trace(eng, tr, src)
+        torch.cuda.synchronize()
+        pay = [capi.tttstate_read_payload(eng.pool, tr.owner(s), l, tr.d_model, tr.d_ff, tr.dtype).tobytes()
+               for s in range(tr.n_streams) for l in range(tr.n_layers)]
+        runs.append((log.versions, {k: v.tobytes() for k, v in src.out.items()}, pay))
+    assert runs[0][0] == runs[1][0]
+    assert runs[0][1] == runs[1][1]
+    assert runs[0][2] == runs[1][2]
