@@ -445,20 +445,28 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
   if (t >= n_tasks) return;
 
   const int target = n + KC;                      // arrivals per output row
-  auto combine = [&](int i) {                     // y_b[i] = Σ_kc base partials + ΔW_b partial (fixed order)
-    if (lane < n) {
-      float y = 0.f;
-      const float dlt = __ldcg(p.Pdelta + (size_t)lane * dm + i);
-      for (int kc0 = 0; kc0 < KC; kc0 += 8) {     // 8 partial loads in flight, summed in kc order
+  // y_b[i] = Σ_kc base partials + ΔW_b partial, in a fixed order: lane (grp, b) = (lane >> 3,
+  // lane & 7) sums slots kc ≡ grp (mod 4) of member b (slot KC = the ΔW partial) with all its
+  // loads in flight at once (one L2 round trip for KC ≤ 31), then two xor shuffles add the groups
+  auto combine = [&](int i) {
+    const int b = lane & 7, grp = lane >> 3;
+    float y = 0.f;
+    if (b < n) {
+      for (int kc0 = grp; kc0 <= KC; kc0 += 32) {
         float part[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          part[e] = kc0 + e < KC ? __ldcg(p.Pbase + ((size_t)(kc0 + e) * kMaxReadMembers + lane) * dm + i) : 0.f;
+        for (int e = 0; e < 8; ++e) {
+          const int kc = kc0 + 4 * e;
+          part[e] = kc < KC ? __ldcg(p.Pbase + ((size_t)kc * kMaxReadMembers + b) * dm + i)
+                            : (kc == KC ? __ldcg(p.Pdelta + (size_t)b * dm + i) : 0.f);
+        }
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (kc0 + e < KC) y += part[e];
+        for (int e = 0; e < 8; ++e) y += part[e];
       }
-      y += dlt;
+    }
+    y += __shfl_xor_sync(0xffffffffu, y, 8);
+    y += __shfl_xor_sync(0xffffffffu, y, 16);
+    if (lane < n) {
       if (p.resid) y += E::to_f(static_cast<const __nv_bfloat16 *>(p.resid)[(size_t)p.y_row[lane] * dm + i]);
       static_cast<__nv_bfloat16 *>(p.Y)[(size_t)p.y_row[lane] * dm + i] = E::from_f(y);
     }
