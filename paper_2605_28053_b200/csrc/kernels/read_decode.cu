@@ -344,6 +344,7 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint3
 }
 
 constexpr int kMmaThreads = 1024, kMmaChunkVec = 64;   // 512 bf16 of K per base task
+constexpr int kXStage = 5;   // x staging loads in flight per thread: 73.9 µs vs 74.5 for the compiler's 4-deep unroll and for 10
 constexpr int kDU = 4;                                  // ΔW loads per lane per batch (= the preloaded batch)
 
 __host__ __device__ inline int mma_nvp(int nvec) { return (nvec + 127) / 128 * 128; }
@@ -421,11 +422,19 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
     row = s_row0[m + 1] + (size_t)(td - m * dm) * nvec;
     load_delta(cur, row, v);
   }
-  for (int idx = tid; idx < kMaxReadMembers * nvp; idx += kMmaThreads) {   // x rows; zero pad / absent members
-    const int b = idx / nvp, vv = idx - b * nvp;
-    xs[idx] = (b < n && vv < nvec)
-                  ? reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff)[vv]
-                  : make_uint4(0u, 0u, 0u, 0u);
+  // x rows (zero pad / absent members): kXStage loads per thread in flight, then the stores
+  for (int base = tid; base < kMaxReadMembers * nvp; base += kXStage * kMmaThreads) {
+    uint4 tmp[kXStage];
+#pragma unroll
+    for (int e = 0; e < kXStage; ++e) {
+      const int idx = base + e * kMmaThreads, b = idx / nvp, vv = idx - b * nvp;
+      tmp[e] = (idx < kMaxReadMembers * nvp && b < n && vv < nvec)
+                   ? reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff)[vv]
+                   : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int e = 0; e < kXStage; ++e)
+      if (base + e * kMmaThreads < kMaxReadMembers * nvp) xs[base + e * kMmaThreads] = tmp[e];
   }
   {                                               // a4 — TailBufferUpdate, spread over every CTA
     const int zq = n * nvec, gtid = blockIdx.x * kMmaThreads + tid, gsz = gridDim.x * kMmaThreads;
