@@ -344,7 +344,7 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint3
 }
 
 constexpr int kMmaThreads = 1024, kMmaChunkVec = 64;   // 512 bf16 of K per base task
-constexpr int kXStage = 5;   // x staging loads in flight per thread: 73.9 µs vs 74.5 for the compiler's 4-deep unroll and for 10
+constexpr int kXStage = 5;   // x staging loads in flight per thread (sweep: 4 = the compiler's unroll, 5, 6, 8, 10; 5 best)
 constexpr int kDU = 4;                                  // ΔW loads per lane per batch (= the preloaded batch)
 
 __host__ __device__ inline int mma_nvp(int nvec) { return (nvec + 127) / 128 * 128; }
