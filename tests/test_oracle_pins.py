@@ -413,3 +413,88 @@ def test_config4_branches_sequential_equals_batched():
         for l in range(tr.n_layers):
             assert all(np.array_equal(x, y) for x, y in zip(S[l], b.branches[br][1][l]))
     assert any(c[4] == "rolled_back" for c in a.commits)
+
+
+# ---------------------------------------------------------------- exact widening
+def test_widen_bf16_exhaustive_against_torch():
+    """Every one of the 65,536 bf16 bit patterns widens exactly as torch's
+    bfloat16 -> float32 -> float64 conversion does (library routine, not a retyped
+    shift).  NaN patterns must stay NaN; everything else must be bit-identical."""
+    bits = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)
+    got = nm.widen(bits, "bf16")
+    ref = torch.from_numpy(bits.view(np.int16).copy()).view(torch.bfloat16).to(torch.float64).numpy()
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(got), nan)
+    assert np.array_equal(got[~nan].view(np.uint64), ref[~nan].view(np.uint64))   # ±0 kept apart
+    # hand values: 0x3F80 = 1.0, 0xC000 = -2.0, 0x0001 = smallest subnormal 2^-133
+    assert nm.widen(np.array([0x3F80, 0xC000, 0x0001], dtype=np.uint16), "bf16").tolist() == \
+        [1.0, -2.0, 2.0 ** -133]
+
+
+def test_widen_fp32_is_exact():
+    rs = np.random.default_rng(11)
+    u = rs.integers(0, 1 << 32, 200_000, dtype=np.uint64).astype(np.uint32)
+    x = u.view(np.float32)
+    got = nm.widen(x, "fp32")
+    ref = torch.from_numpy(x.copy()).to(torch.float64).numpy()
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(got), nan)
+    assert np.array_equal(got[~nan].view(np.uint64), ref[~nan].view(np.uint64))
+
+
+# ---------------------------------------------------------------- pre-filled tails (reading xv)
+def test_prefill_tail_hand_worked_bursty_example():
+    """A stream that starts with 2 of C = 3 evidence entries already in its tail
+    (bursty start, reading xv; "the tail holds the chunk's evidence").
+
+    Worked by hand (d_model = 1, d_ff = 2, W_down = [1, 1], η = 1/2, ΔW_0 = 0):
+      pre-filled  p = -2: z = (1, 0), v = 2;   p = -1: z = (0, 1), v = 1
+      decode      p =  0: z = (1, 1), v = -1  -> tail holds C-1 = 2 before it: WRITE
+                  y_0 = (W + ΔW_0) z = 2  (pre-update version, reading xvii)
+                  ΔW_1 = η (2·(1,0) + 1·(0,1) − 1·(1,1)) = (1/2, 0),  v: 0 -> 1
+      decode      p =  1: z = (2, 0), v = 1   -> READ,  y_1 = (1.5, 1)·(2, 0) = 3
+                  p =  2: z = (0, 2), v = 1   -> READ,  y_2 = 2
+                  p =  3: z = (1, 0), v = 1   -> WRITE, y_3 = 1.5 (pre-update), then
+                  ΔW_2 = ΔW_1 + η (1·(2,0) + 1·(0,2) + 1·(1,0)) = (2, 1)
+    """
+    tab = StateTable(1, 1, 2, 3, "fp32", [np.array([[1.0, 1.0]])], 0.5)
+    tab.alloc(7)
+    tab.prefill_tail(7, [[np.array([1.0, 0.0])], [np.array([0.0, 1.0])]],
+                     [[np.array([2.0])], [np.array([1.0])]], [-2, -1])
+    assert tab.tail_len(7) == 2
+    steps = [((1.0, 1.0), -1.0), ((2.0, 0.0), 1.0), ((0.0, 2.0), 1.0), ((1.0, 0.0), 1.0)]
+    effects, ys = [], []
+    for p, (z, v) in enumerate(steps):
+        eff = tab.next_effect(7)
+        effects.append(eff)
+        ys.append(float(tab.apply(7, p, [np.array(z)], [np.array([v])])[0][0]))
+        if eff == WRITE:
+            tab.write_group([7])
+            if p == 0:
+                assert tab.owners[7].S[0].tolist() == [[0.5, 0.0]] and tab.version(7) == 1
+    assert effects == [WRITE, READ, READ, WRITE]
+    assert ys == [2.0, 3.0, 2.0, 1.5]     # p=2: (1.5,1)·(0,2) = 2; p=3: (1.5,1)·(1,0) = 1.5
+    assert tab.owners[7].S[0].tolist() == [[2.0, 1.0]] and tab.version(7) == 2
+
+
+def test_prefill_tail_bursty_trace_first_write_and_closed_form():
+    """Through the trace driver (init_stream -> prefill_tail) on a bursty trace:
+    stream s's first WRITE is at p = C-1-offset_s, every later one C steps apart,
+    and the committed ΔW equals the closed form over pre-filled + decoded evidence
+    η·Σ_{p=-off..last committed} v_p z_pᵀ (P:299-308 target = sequential execution)."""
+    C = 4
+    offs = (0, 1, 2, 3)
+    tr = T.uniform_small(n_streams=4, n_layers=1, d_model=3, d_ff=5, chunk=C, n_steps=11, dtype="fp32")
+    tr = tr.replace(offsets=offs, eta=2.0 ** -3)
+    rec = run_sequential(tr)
+    for s, off in enumerate(offs):
+        writes = [p for p in range(tr.n_steps) if rec.events[(s, p)] == WRITE]
+        assert writes == list(range(C - 1 - off, tr.n_steps, C))
+        last = writes[-1]
+        Z = np.stack([nm.widen(tr.x(s, p, 0), "fp32") for p in range(-off, last + 1)])
+        Vt = np.stack([nm.widen(tr.tgt(s, p, 0), "fp32") for p in range(-off, last + 1)])
+        closed = tr.eta * (Vt.T @ Z)
+        assert rec.versions[s] == len(writes)
+        # fp32 storage rounds once per commit: agreement to fp32 precision, while a
+        # dropped or duplicated evidence entry moves the state by ~η·|v||z| ≫ 1e-6.
+        assert nm.normwise_rel_err(rec.state[s][0], closed) < 1e-6
