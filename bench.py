@@ -211,7 +211,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2605_28053_b200 import capi
-    from paper_2605_28053_b200.serving import Engine, InputSource, Server
+    from paper_2605_28053_b200.serving import Engine, InputSource, Server, StepIO
     from workload import rng
     from workload import traces as T
 
@@ -276,6 +276,11 @@ def main():
             rows = self._rows
             return self.X[l], rows, self.V[l], rows, self.Y[l], rows
 
+        def step_io(self, ss, ps):               # the native step: one row map for every layer
+            rows = [(p % CHUNK) * N_STREAMS + s for s, p in zip(ss, ps)]
+            return StepIO(self.X, CHUNK * N_STREAMS * D_FF, self.V, CHUNK * N_STREAMS * D_MODEL, self.Y,
+                          CHUNK * N_STREAMS * D_MODEL, rows)
+
     # start of run: rank 0's config and owner→rank map to every rank; each
     # rank checks that the owners it serves are exactly the ones the map places on it
     run_cfg = D.broadcast_config({"n_streams_per_rank": N_STREAMS, "layers": L, "chunk": CHUNK,
@@ -285,7 +290,7 @@ def main():
         [tr.owner(s) for s in range(N_STREAMS)], "owner map disagrees with this rank's owners"
     src = Window()
     stream = torch.cuda.current_stream(dev)
-    srv = Server(eng, tr, src, stream=stream, sync_writes=True, profile=True, profile_every=8)
+    srv = Server(eng, tr, src, stream=stream, profile=True, profile_every=8)
     srv.admit()
     torch.cuda.synchronize(dev)
     del src.d0

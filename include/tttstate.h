@@ -22,13 +22,29 @@
  *    definition has run the update and *not* committed it.
  *  - Device pointers are stream-ordered on the `stream` argument (a
  *    cudaStream_t passed as void*, NULL = legacy default stream).  No call
- *    blocks the host except tttstate_sync, tttstate_read_payload and
- *    tttstate_read_tail (test hooks).  All compute calls on one pool must be
- *    issued on one stream (or otherwise serialised): a pool owns one device
- *    workspace.
+ *    blocks the host except tttstate_sync, tttstate_refusals and the test hooks
+ *    (read_payload / read_slot_raw / read_tail / device_version), and — only
+ *    while an earlier write_commit of the same owner is still unconfirmed —
+ *    the calls that confirm it (see "Commit confirmation" below).  All compute
+ *    calls on one pool must be issued on one stream (or otherwise serialised):
+ *    a pool owns one device workspace.
  *  - Ownership: the caller owns the device arena, W_down, X, targets, Y and
  *    streams; the library never allocates device memory.  The pool owns the
- *    slot assignment, tails, version tables and checkpoints inside the arena.
+ *    slot assignment, tails, version tables and checkpoints inside the arena,
+ *    plus a small pinned device-mapped HOST block (24 B per owner) into which
+ *    the commit kernel writes each member's post-commit (version, slot).
+ *  - Commit confirmation.  write_commit never waits for its kernels: the host
+ *    mirror moves every member to v+1 at once (no host sync on the decode
+ *    path).  The device may still refuse a member whose candidate is not
+ *    finite (App. H fallback resolved on the device, reading xx):
+ *    that member keeps v and its committed bytes, and its chunk's evidence is
+ *    dropped.  An owner's latest commit is "confirmed" (the mirror corrected
+ *    from the device's record, waiting on that commit's event, normally long
+ *    complete) by every call that relies on its committed version or slot:
+ *    tttstate_version, tttstate_snapshot, rollback, tttstate_fork (source),
+ *    write_commit / fused read_apply of an owner holding a checkpoint, and
+ *    tttstate_sync (all owners).  READ launches use the device slot table, so
+ *    they always see the device's committed state.
  *  - Layouts are row-major.  Element type of every operand (ΔW, W_down, X,
  *    targets, Y, residual) is the pool's σ.dtype: TTT_BF16 (uint16 bf16
  *    bits) or TTT_FP32.  Accumulation is fp32 in every kernel.
@@ -75,7 +91,9 @@ enum { TTT_FAST_WEIGHT = 0, TTT_LOW_RANK = 1, TTT_STREAMING = 2 }; /* τ */
 enum { TTT_MODE_SERIAL = 0, TTT_MODE_PHASE = 1, TTT_MODE_FULL = 2 };
 
 /* τ + σ of one pool.  rule 0: ΔW += η·V_cᵀZ_c (reading i).
- * backend must be TTT_FAST_WEIGHT in this version; rank is 0.            */
+ * backend: TTT_FAST_WEIGHT (rank 0) or TTT_LOW_RANK (NEXT f1: payload A
+ * [rank][d_ff] then B [rank][d_model] per layer, bf16, 1 <= rank <= 64).
+ * Only rule 0 runs on the GPU.                                           */
 typedef struct {
   int32_t backend, dtype, d_model, d_ff, chunk, rank, n_layers, rule;
 } ttt_shape;
@@ -202,11 +220,15 @@ ttt_status tttstate_step_done(ttt_pool *pool, const ttt_group *g);
  * member's shadow slot (fp32 accumulate, one rounding to σ.dtype); then one
  * commit kernel publishes active ^= 1, V += 1 for all members iff no member
  * failed (fail_mask bit b set = injected failure of member b; a non-finite
- * candidate element = device-detected failure).  On success tails are
- * cleared and new_versions[b] (host, may be NULL) = v+1.  An injected
- * failure returns TTT_E_WRITE_FAILED with versions, committed bytes and
- * tails intact (retry as singletons, App. H fallback).  A device-detected
- * failure is reported by the next tttstate_sync.  fail_mask: host array of
+ * candidate element = device-detected failure).  On return tails are
+ * cleared and new_versions[b] (host, may be NULL) = v+1 — provisional until
+ * confirmed (header "Commit confirmation").  An injected failure returns
+ * TTT_E_WRITE_FAILED with versions, committed bytes and tails intact (the
+ * caller retries as singletons, App. H fallback).  A
+ * device-detected failure fails the group on the device, which resolves the
+ * singleton retries at once: members with finite candidates commit (their
+ * retry would write the same bytes), the others keep v (refusal records:
+ * tttstate_refusals; counted by tttstate_sync).  fail_mask: host array of
  * ceil(n/32) words or NULL.                                                 */
 ttt_status write_commit(ttt_pool *pool, const ttt_group *g, float eta, const uint32_t *fail_mask,
                         uint64_t *new_versions, void *stream);
@@ -219,11 +241,74 @@ ttt_status rollback(ttt_pool *pool, uint64_t owner, uint64_t *v_out, void *strea
 /* a7 — new lineage dst from src's committed state, same v, empty tail (reading viii). */
 ttt_status tttstate_fork(ttt_pool *pool, uint64_t src, uint64_t dst, void *stream);
 
-/* Synchronise `stream` and reconcile device-detected write failures with the
- * host mirror.  Returns TTT_E_WRITE_FAILED (and n_failed_out > 0) if a group
- * failed on the device since the last sync; those owners are back at their
- * pre-write version with their full tail retained.                          */
+/* Synchronise `stream` and confirm every pending commit.  Returns
+ * TTT_E_WRITE_FAILED (and n_failed_out > 0) if groups had members refused on
+ * the device since the last sync; those members are at the version they
+ * kept, with empty tails.                                                    */
 ttt_status tttstate_sync(ttt_pool *pool, void *stream, int32_t *n_failed_out);
+/* Drain the device refusal records (synchronises `stream`): for each member the
+ * device refused, its owner id, the version it kept and the commit sequence
+ * number of the write_commit that ran it (tttstate_last_commit_seq).  Returns
+ * at most cap records per call, oldest first; TTT_E_CAPACITY if more than
+ * 4096 records accumulated between drains.                                   */
+ttt_status tttstate_refusals(ttt_pool *pool, uint64_t *owners, uint64_t *versions, uint64_t *seqs,
+                             int32_t cap, int32_t *n_out, void *stream);
+/* Sequence number of the pool's latest successful write_commit (0 before any). */
+ttt_status tttstate_last_commit_seq(ttt_pool *pool, uint64_t *seq_out);
+
+/* ------------------------------------------------------- one serving step */
+/* Inputs/outputs of one decode step: the token of owners[i] sits at row rows[i]
+ * of every layer's X [*, d_ff], Vt [*, d_model], Y / resid [*, d_model]; layer
+ * l's matrices start x/v/y/r_layer_stride ELEMENTS after layer l−1's.  Device
+ * memory, σ.dtype.  rows == NULL: row i.  resid may be NULL.                 */
+typedef struct {
+  const void *X;
+  int64_t x_layer_stride;
+  const void *Vt;
+  int64_t v_layer_stride;
+  void *Y;
+  int64_t y_layer_stride;
+  const void *resid;
+  int64_t r_layer_stride;
+  const int32_t *rows;
+  void *ev_write_begin, *ev_write_end;   /* profiling (may be NULL): cudaEvent_t recorded right before the
+                                          * step's first WRITE group's WRITE launches and after its commit */
+} ttt_step_io;
+
+/* Host buffers the step fills (caller-owned).  groups/owner_buf as plan_batch;
+ * v_before[j] (may be NULL) = the version issued member j's token used;
+ * member_seq[j] (may be NULL) = the commit sequence number that published (or
+ * tried to publish) member j's WRITE, 0 for READ members; injected[k] (may be
+ * NULL) = 1 if WRITE group k hit an injected failure and ran the singleton
+ * fallback.  Members are numbered in owner_buf order.                          */
+typedef struct {
+  ttt_group *groups;
+  int32_t group_cap;
+  int32_t owner_cap;
+  uint64_t *owner_buf;
+  uint64_t *v_before;
+  uint64_t *member_seq;
+  int32_t *injected;
+  int32_t rej_cap;
+  int32_t _pad;
+  ttt_event *rejected;
+  int32_t n_groups, n_rejected, n_read, n_write, n_injected, _pad2;
+} ttt_step_out;
+
+/* One iteration of Alg. 1 for the owners listed, in one call (no
+ * per-layer host round trips, no host sync — SURVEY App. B "Launch and
+ * overhead"):  a1 NextStep for every listed owner without an event pending in
+ * the planner (w > 0 holds events across steps) -> a2 plan_batch at `clock`
+ * (rejected events are returned, never issued; re-extract them next step) ->
+ * for every group, L dependent read_apply launches (a3 + a4) -> READ groups:
+ * step done; WRITE groups: write_commit (a5 + a6, η = eta).  Owners in
+ * fail_owners get an injected WRITE failure on this step's first attempt; such
+ * a group is retried as serial singletons in μ order (App. H).
+ * Validation (owners known and distinct, buffers, planner capacity) happens
+ * before any side effect; a CUDA error after launches began returns TTT_E_CUDA. */
+ttt_status tttstate_serve_step(ttt_pool *pool, ttt_planner *pl, const uint64_t *owners, int32_t n, int64_t clock,
+                               const ttt_step_io *io, float eta, const uint64_t *fail_owners, int32_t n_fail,
+                               ttt_step_out *out, void *stream);
 
 /* Test hooks (blocking): committed ΔW[layer] of owner -> host [d_model][d_ff];
  * tail entries -> host Z [C][d_ff], V [C][d_model]; device version table.    */

@@ -121,12 +121,25 @@ def run_sequential(tr: Trace, layers=None, keep_outputs: bool = True, streams=No
                         tab.write_group([r], fail=True)
                     except ContractError:
                         rec.commits.append((s, p, v, v, "failed"))
-                tab.write_group([r])
-                rec.commits.append((s, p, v, v + 1, "ok"))
+                _retry(tab, rec, r, s, p, v)
         rec.versions[s] = tab.version(r)
         rec.state[s] = _state_copy(tab.owners[r].S)
     _branches(tab, tr, rec)
     return rec
+
+
+def _retry(tab, rec, r, s, p, v):
+    """A singleton WRITE (App. H fallback).  A non-finite candidate fails it
+    again — the update is deterministic — so that failure is final: v and ΔW stay and the
+    chunk's evidence is dropped (reading xx)."""
+    try:
+        tab.write_group([r])
+        rec.commits.append((s, p, v, v + 1, "ok"))
+    except ContractError as e:
+        if e.code != "WRITE_FAILED":
+            raise
+        tab.drop_chunk(r)
+        rec.commits.append((s, p, v, v, "failed"))
 
 
 def _state_copy(S):
@@ -186,8 +199,7 @@ def run_batched(tr: Trace, layers=None, keep_outputs: bool = True) -> Record:
                         failed_once.add((s, pos[s]))
                         rec.commits.append((s, pos[s], vb[s], vb[s], "failed"))
                     for s in ss:                            # fallback: serial singletons in μ order
-                        tab.write_group([tr.owner(s)])
-                        rec.commits.append((s, pos[s], vb[s], vb[s] + 1, "ok"))
+                        _retry(tab, rec, tr.owner(s), s, pos[s], vb[s])
             for s in ss:                                    # UpdateKVAndTailMetadata
                 pos[s] += 1
                 pending.discard(s)

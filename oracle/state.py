@@ -171,6 +171,13 @@ class StateTable:
         self.owners[dst] = Owner(v=o.v, S=_copy(o.S))
         return o.v
 
+    def drop_chunk(self, r: int):
+        """A WRITE that failed for good (its singleton retry failed too: a non-finite candidate
+        fails the same way every time): v and ΔW stay, the chunk's evidence is discarded
+        (tail cleared, as rollback does — reading vii; reading xx)."""
+        o = self._get(r)
+        o.tail_z, o.tail_v, o.tail_p = [], [], []
+
     def prefill_tail(self, r: int, zs_list: list, vs_list: list, ps: list):
         """Seed a partially-filled tail (bursty starts, reading xv)."""
         o = self._get(r)

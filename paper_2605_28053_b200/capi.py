@@ -52,6 +52,21 @@ class ttt_group(C.Structure):
                 ("owner_map", C.POINTER(C.c_uint64)), ("issue_step", C.c_int64)]
 
 
+class ttt_step_io(C.Structure):
+    _fields_ = [("X", C.c_void_p), ("x_layer_stride", C.c_int64), ("Vt", C.c_void_p), ("v_layer_stride", C.c_int64),
+                ("Y", C.c_void_p), ("y_layer_stride", C.c_int64), ("resid", C.c_void_p), ("r_layer_stride", C.c_int64),
+                ("rows", C.POINTER(C.c_int32)), ("ev_write_begin", C.c_void_p), ("ev_write_end", C.c_void_p)]
+
+
+class ttt_step_out(C.Structure):
+    _fields_ = [("groups", C.POINTER(ttt_group)), ("group_cap", C.c_int32), ("owner_cap", C.c_int32),
+                ("owner_buf", C.POINTER(C.c_uint64)), ("v_before", C.POINTER(C.c_uint64)),
+                ("member_seq", C.POINTER(C.c_uint64)), ("injected", C.POINTER(C.c_int32)),
+                ("rej_cap", C.c_int32), ("_pad", C.c_int32), ("rejected", C.POINTER(ttt_event)),
+                ("n_groups", C.c_int32), ("n_rejected", C.c_int32), ("n_read", C.c_int32), ("n_write", C.c_int32),
+                ("n_injected", C.c_int32), ("_pad2", C.c_int32)]
+
+
 assert C.sizeof(ttt_event) == 40 and C.sizeof(ttt_shape) == 32
 
 
@@ -95,6 +110,11 @@ _sigs = {
     "rollback": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_uint64), P]),
     "tttstate_fork": (C.c_int, [P, C.c_uint64, C.c_uint64, P]),
     "tttstate_sync": (C.c_int, [P, P, C.POINTER(C.c_int32)]),
+    "tttstate_refusals": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                    C.c_int32, C.POINTER(C.c_int32), P]),
+    "tttstate_last_commit_seq": (C.c_int, [P, C.POINTER(C.c_uint64)]),
+    "tttstate_serve_step": (C.c_int, [P, P, C.POINTER(C.c_uint64), C.c_int32, C.c_int64, C.POINTER(ttt_step_io),
+                                      C.c_float, C.POINTER(C.c_uint64), C.c_int32, C.POINTER(ttt_step_out), P]),
     "tttstate_read_payload": (C.c_int, [P, C.c_uint64, C.c_int32, P, P]),
     "tttstate_read_slot_raw": (C.c_int, [P, C.c_uint64, C.c_int32, C.c_int32, P, P]),
     "tttstate_read_tail": (C.c_int, [P, C.c_uint64, C.c_int32, P, P, P]),
@@ -130,6 +150,32 @@ def _stream(s):
     if isinstance(s, int):
         return s
     return s.cuda_stream
+
+
+_POOL_INFO: dict = {}     # pool handle -> ttt_shape (argument checks of tensor operands)
+_TORCH_DTYPE = {FP32: "torch.float32", BF16: "torch.bfloat16"}
+
+
+def _check_tensor(t, what: str, pool, last: int | None = None, min_rows: int = 0):
+    """Checks a torch-tensor operand against the pool's σ.dtype / row width (raw integer
+    addresses are the caller's opt-in unchecked path)."""
+    if t is None or isinstance(t, int) or pool not in _POOL_INFO:
+        return
+    sh = _POOL_INFO[pool]
+    if str(t.dtype) != _TORCH_DTYPE[sh.dtype]:
+        raise ValueError(f"{what}: dtype {t.dtype} does not match the pool's {_TORCH_DTYPE[sh.dtype]}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: must be contiguous (row-major)")
+    if last is not None and (t.dim() == 0 or t.shape[-1] != last):
+        raise ValueError(f"{what}: last dimension {tuple(t.shape)[-1:]} != {last}")
+    rows = t.numel() // last if last else 0
+    if min_rows and rows < min_rows:
+        raise ValueError(f"{what}: {rows} rows < {min_rows} needed")
+
+
+def _check_rows(rows, n: int, what: str):
+    if rows is not None and len(rows) < n:
+        raise ValueError(f"{what}: {len(rows)} row indices for a group of {n}")
 
 
 def _rows(rows):
@@ -190,14 +236,24 @@ def tttstate_pool_create(shape: ttt_shape, shape_id: int, placement: int, max_ow
     out = P()
     _check(_lib.tttstate_pool_create(C.byref(shape), shape_id, placement, max_owners, n_ckpt, _ptr(dev_arena),
                                      arena_bytes, _ptr(w_down), C.byref(out)))
+    _POOL_INFO[out.value] = ttt_shape.from_buffer_copy(shape)
+    if shape.rule == 0:
+        _check_tensor(w_down, "w_down", out.value, shape.d_ff, shape.n_layers * shape.d_model)
     return out.value
 
 
 def tttstate_pool_destroy(pool):
+    _POOL_INFO.pop(pool, None)
     _check(_lib.tttstate_pool_destroy(pool))
 
 
 def tttstate_alloc(pool, owner: int, init=None, v0: int = 0, stream=None) -> int:
+    if pool in _POOL_INFO and init is not None and not isinstance(init, int):
+        sh = _POOL_INFO[pool]
+        per = sh.rank * (sh.d_ff + sh.d_model) if sh.backend == LOW_RANK else sh.d_model * sh.d_ff
+        _check_tensor(init, "init", pool)
+        if init.numel() < sh.n_layers * per:
+            raise ValueError(f"init: {init.numel()} elements < {sh.n_layers * per}")
     v = C.c_uint64()
     _check(_lib.tttstate_alloc(pool, owner, _ptr(init), v0, C.byref(v), _stream(stream)))
     return v.value
@@ -208,6 +264,10 @@ def tttstate_free(pool, owner: int):
 
 
 def tttstate_tail_load(pool, owner: int, n: int, Z, V, stream=None):
+    if pool in _POOL_INFO and n > 0:
+        sh = _POOL_INFO[pool]
+        _check_tensor(Z, "Z", pool, sh.d_ff, sh.n_layers * n)
+        _check_tensor(V, "V", pool, sh.d_model, sh.n_layers * n)
     _check(_lib.tttstate_tail_load(pool, owner, n, _ptr(Z), _ptr(V), _stream(stream)))
 
 
@@ -284,12 +344,25 @@ def validate_group(pool, group: Group, expected_versions=None):
 
 # ---------------------------------------------------------------- operators
 def read_apply(pool, group: Group, layer: int, X, x_rows, Vt, v_rows, Y, y_rows=None, resid=None, stream=None):
+    if pool in _POOL_INFO:
+        sh, n = _POOL_INFO[pool], len(group)
+        _check_tensor(X, "X", pool, sh.d_ff, 0 if x_rows is not None else n)
+        _check_tensor(Vt, "Vt", pool, sh.d_model, 0 if v_rows is not None else n)
+        _check_tensor(Y, "Y", pool, sh.d_model, 0 if y_rows is not None else n)
+        _check_tensor(resid, "resid", pool, sh.d_model)
+        for r, w in ((x_rows, "x_rows"), (v_rows, "v_rows"), (y_rows, "y_rows")):
+            _check_rows(r, n, w)
     _check(_lib.read_apply(pool, C.byref(group.c), layer, _ptr(X), _rows(x_rows), _ptr(Vt), _rows(v_rows),
                            _ptr(Y), _rows(y_rows), _ptr(resid), _stream(stream)))
 
 
 def read_apply_chunk(pool, group: Group, layer: int, X, Vt, Y, stream=None):
     """NEXT f2: all C tokens of each member's chunk at version v (tcgen05); then write_commit."""
+    if pool in _POOL_INFO:
+        sh, n = _POOL_INFO[pool], len(group)
+        _check_tensor(X, "X", pool, sh.d_ff, n * sh.chunk)
+        _check_tensor(Vt, "Vt", pool, sh.d_model, n * sh.chunk)
+        _check_tensor(Y, "Y", pool, sh.d_model, n * sh.chunk)
     _check(_lib.read_apply_chunk(pool, C.byref(group.c), layer, _ptr(X), _ptr(Vt), _ptr(Y), _stream(stream)))
 
 
@@ -336,6 +409,72 @@ def tttstate_sync(pool, stream=None) -> int:
     if st not in (TTT_OK, TTT_E_WRITE_FAILED):
         _check(st)
     return n.value
+
+
+def tttstate_refusals(pool, stream=None, cap: int = 4096):
+    """Drain the device refusal records: list of (owner, version kept, commit seq)."""
+    o, v, q = (C.c_uint64 * cap)(), (C.c_uint64 * cap)(), (C.c_uint64 * cap)()
+    n = C.c_int32()
+    _check(_lib.tttstate_refusals(pool, o, v, q, cap, C.byref(n), _stream(stream)))
+    return [(o[k], v[k], q[k]) for k in range(n.value)]
+
+
+def tttstate_last_commit_seq(pool) -> int:
+    v = C.c_uint64()
+    _check(_lib.tttstate_last_commit_seq(pool, C.byref(v)))
+    return v.value
+
+
+class StepBuffers:
+    """Preallocated host buffers of tttstate_serve_step (reused every step: marshalling only)."""
+
+    def __init__(self, max_owners: int, group_cap: int = 256):
+        self.owners = (C.c_uint64 * max(1, max_owners))()
+        self.rows = (C.c_int32 * max(1, max_owners))()
+        self.fail = (C.c_uint64 * max(1, max_owners))()
+        self.groups = (ttt_group * group_cap)()
+        self.owner_buf = (C.c_uint64 * max(1, max_owners))()
+        self.v_before = (C.c_uint64 * max(1, max_owners))()
+        self.member_seq = (C.c_uint64 * max(1, max_owners))()
+        self.injected = (C.c_int32 * group_cap)()
+        self.rejected = (ttt_event * max(1, max_owners))()
+        self.io = ttt_step_io()
+        self.io.rows = C.cast(self.rows, C.POINTER(C.c_int32))
+        self.out = ttt_step_out(self.groups, group_cap, max(1, max_owners), self.owner_buf, self.v_before,
+                                self.member_seq, self.injected, max(1, max_owners), 0, self.rejected)
+
+    def groups_issued(self):
+        """[(effect, [owners], [v_before], [member_seq], injected)] of the last step."""
+        res, off = [], 0
+        for k in range(self.out.n_groups):
+            g = self.groups[k]
+            res.append((g.effect, list(self.owner_buf[off:off + g.n]), list(self.v_before[off:off + g.n]),
+                        list(self.member_seq[off:off + g.n]), bool(self.injected[k])))
+            off += g.n
+        return res
+
+
+def tttstate_serve_step(pool, pl, bufs: StepBuffers, n: int, clock: int, X, x_stride, Vt, v_stride, Y, y_stride,
+                        eta: float, n_fail: int = 0, resid=None, r_stride: int = 0, stream=None,
+                        ev_write=(None, None)):
+    """One Alg. 1 iteration for bufs.owners[:n] at rows bufs.rows[:n] (fill those arrays first)."""
+    if pool in _POOL_INFO:
+        sh = _POOL_INFO[pool]
+        rmax = 1 + max((bufs.rows[i] for i in range(n)), default=-1)
+        for t, w, last, stride in ((X, "X", sh.d_ff, x_stride), (Vt, "Vt", sh.d_model, v_stride),
+                                   (Y, "Y", sh.d_model, y_stride)):
+            _check_tensor(t, w, pool, last)
+            if t is not None and not isinstance(t, int) and \
+                    t.numel() < (sh.n_layers - 1) * stride + rmax * last:
+                raise ValueError(f"{w}: too small for {sh.n_layers} layers at stride {stride} and row {rmax - 1}")
+    io = bufs.io
+    io.X, io.x_layer_stride, io.Vt, io.v_layer_stride = _ptr(X), x_stride, _ptr(Vt), v_stride
+    io.Y, io.y_layer_stride, io.resid, io.r_layer_stride = _ptr(Y), y_stride, _ptr(resid), r_stride
+    io.ev_write_begin = None if ev_write[0] is None else ev_write[0].cuda_event
+    io.ev_write_end = None if ev_write[1] is None else ev_write[1].cuda_event
+    _check(_lib.tttstate_serve_step(pool, pl, bufs.owners, n, clock, C.byref(io), C.c_float(eta),
+                                    bufs.fail if n_fail else None, n_fail, C.byref(bufs.out), _stream(stream)))
+    return bufs.out
 
 
 def _np_dtype(dtype):

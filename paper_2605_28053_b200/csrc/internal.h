@@ -34,7 +34,7 @@ struct ReadParams {
   int tail_pos[kMaxReadMembers];
   int fuse;                      // f3: also write ΔW + η·v·xᵀ to the shadow slot (C = 1)
   float eta;
-  int *fail_flag;
+  int *mfail;                    // [max_owners] per-owner device-failure flags (non-finite candidate)
   int order;                     // task order: 0 CTA-major, 1 SM-interleaved (balanced bytes per SM)
   int dyn;                       // per-CTA dynamic task hand-out (SM-interleaved order only)
   int kc;                        // > 0: tensor-core base (bf16), Pbase holds kc K-chunk slabs [kc][8][d_model]
@@ -49,21 +49,39 @@ struct WriteParams {
   const void *tailZ, *tailV;
   long long tz_owner, tv_owner, tz_layer, tv_layer;
   float eta;
-  int *fail_flag;
+  int *mfail;                    // [max_owners] per-owner device-failure flags (non-finite candidate)
   int n, d_model, d_ff, C;
   int max_owners, max_slots;     // tensor-map extents (tails, pool slots)
   int owner_idx[kMaxGroup];
 };
 
-// a6: group-atomic publish.
+// Post-commit state of one owner, written by the commit kernel into pinned device-mapped
+// host memory (read by the host only after the commit's event completed).
+struct HostOwnerState {
+  unsigned long long version, seq;
+  int sel, pad;
+};
+// One device-refused member (non-finite candidate), appended by the commit kernel.
+struct RefusalRec {
+  unsigned long long owner, version, seq;   // owner id, version it stays at, commit sequence number
+  unsigned long long pad;
+};
+constexpr int kRefusalLog = 4096;          // records kept in the device ring (drained by tttstate_refusals)
+
+// a6: group commit with the App. H fallback resolved on the device.
 struct CommitParams {
   int *sel;
   unsigned long long *version;
-  int *fail_flag;      // device-detected failure flag of the current group (reset here)
-  int *fail_count;     // cumulative device-detected failed groups (read by tttstate_sync)
-  int forced_fail;     // injected failure (host-known)
+  int *mfail;          // [max_owners] per-owner device-failure flags set by the WRITE kernels (cleared here)
+  int *fail_count;     // cumulative groups with a device-refused member (read by tttstate_sync)
+  int *rlog_count;     // refusal-log append counter
+  RefusalRec *rlog;    // [kRefusalLog] ring
+  HostOwnerState *hstate;   // mapped host [max_owners]: post-commit (version, sel, seq)
+  unsigned long long seq;   // this commit's sequence number
+  int forced_fail;     // injected failure (host-known): nothing publishes
   int n;
   int owner_idx[kMaxGroup];
+  unsigned long long owner_id[kMaxGroup];
   int partial;         // test hook (TTT_HOOK_NO_GROUP_ATOMICITY): publish members with no fail bit
   unsigned fail_bits[kMaxGroup / 32];
 };
@@ -115,7 +133,7 @@ struct LowRankWrite {
   const void *tailZ;
   long long tz_owner, tz_layer;
   float eta;
-  int *fail_flag;
+  int *mfail;                    // [max_owners] per-owner device-failure flags (non-finite candidate)
   int owner_idx[kMaxGroup];
 };
 bool read_chunk_fused_fits(int row_blocks, int d_model, int ksplit);
@@ -136,7 +154,7 @@ cudaError_t launch_write_tc(const WriteParams &p, cudaStream_t s);   // bf16, tc
 bool write_tc_supported(int d_model, int d_ff, int C);
 cudaError_t launch_commit(const CommitParams &p, cudaStream_t s);
 cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s);
-cudaError_t launch_set_state(int *sel, unsigned long long *version, int idx, int sel_v,
+cudaError_t launch_set_state(int *sel, unsigned long long *version, int *mfail, int idx, int sel_v,
                              unsigned long long ver, cudaStream_t s);
 
 void count_launch(int n = 1);

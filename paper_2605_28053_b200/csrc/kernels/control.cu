@@ -3,11 +3,22 @@
 // Commit: "Commit publishes a dirty state
 // as owner r's next version only after the WRITE group succeeds ... The
 // version counter changes here, not inside the backend update".  Group-atomic
-// (SURVEY.md §8(c) reading vi): one CTA reads the group's
-// fail flag once, then every member flips its active slot and bumps its
-// version, or none does.  No payload bytes move (the dirty candidate already
-// sits in the shadow slot), replacing the paper's "selective commit" copy
-// kernel with an O(1)-per-owner publish.
+// (SURVEY.md §8(c) reading vi) with App. H's fallback
+// (a failed group is retried as serial singletons) resolved on the
+// device, so the host never waits for a WRITE's outcome:
+//   * an injected failure (host-known) publishes nothing; the host retries;
+//   * a device-detected failure (non-finite candidate, per-owner flag raised by
+//     the WRITE kernels) fails the group as a whole, and its singleton retries
+//     are decided here at once: a member's candidate does not depend on the
+//     other members (same committed state, same evidence, same kernel), so the
+//     retry of a clean member would write the very bytes already sitting in its
+//     shadow slot — it is published; a flagged member's retry would fail the
+//     same way — it is refused for good (v and bytes intact, its chunk's
+//     evidence dropped: DESIGN.md reading xx), and a refusal record is logged.
+// No payload bytes move (the dirty candidate already sits in the shadow slot),
+// replacing the paper's "selective commit" copy kernel with an
+// O(1)-per-owner publish.  Every member's post-commit (version, sel, seq) is
+// written to pinned device-mapped host memory for the host's lazy confirmation.
 //
 // Checkpoint copy ("Checkpoint write", K5): a 16-byte vectorised
 // device copy used when a pinned checkpoint slot must be preserved, for
@@ -18,22 +29,42 @@ namespace ttt {
 namespace {
 
 __global__ void commit_kernel(const CommitParams p) {
-  __shared__ int fail;
-  if (threadIdx.x == 0) fail = p.forced_fail | *reinterpret_cast<volatile int *>(p.fail_flag);
-  __syncthreads();
-  if (!fail || p.partial) {                      // p.partial: test hook only (negative control)
-    for (int b = threadIdx.x; b < p.n; b += blockDim.x) {
-      if (fail && ((p.fail_bits[b / 32] >> (b % 32)) & 1u)) continue;
-      const int o = p.owner_idx[b];
+  int bad_any = 0;
+  for (int b = threadIdx.x; b < p.n; b += blockDim.x) {
+    const int o = p.owner_idx[b];
+    const int bad = *reinterpret_cast<volatile int *>(p.mfail + o);
+    if (p.forced_fail) {                         // injected: the host runs the singleton retries
+      // (the flag stays: a fused C = 1 candidate is not recomputed by its retry; rollback /
+      // alloc / fork clear it through set_state_kernel)
+      if (p.partial && !((p.fail_bits[b / 32] >> (b % 32)) & 1u)) {   // test hook (negative control)
+        p.sel[o] ^= 1;
+        p.version[o] += 1ull;
+      }
+      continue;
+    }
+    p.mfail[o] = 0;                              // resolved here; the next WRITE raises it again if it must
+    if (!bad) {
       p.sel[o] ^= 1;
       p.version[o] += 1ull;
+    } else {
+      const int k = atomicAdd(p.rlog_count, 1);
+      RefusalRec r;
+      r.owner = p.owner_id[b];
+      r.version = p.version[o];
+      r.seq = p.seq;
+      r.pad = 0;
+      p.rlog[k % kRefusalLog] = r;
     }
+    bad_any |= bad;
+    HostOwnerState h;
+    h.version = p.version[o];
+    h.seq = p.seq;
+    h.sel = p.sel[o];
+    h.pad = 0;
+    p.hstate[o] = h;                             // posted writes into mapped host memory
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (fail && !p.forced_fail) atomicAdd(p.fail_count, 1);
-    *p.fail_flag = 0;
-  }
+  if (__syncthreads_or(bad_any) && threadIdx.x == 0) atomicAdd(p.fail_count, 1);
+  __threadfence_system();
 }
 
 __global__ void copy_kernel(uint4 *__restrict__ dst, const uint4 *__restrict__ src, size_t n16) {
@@ -50,10 +81,11 @@ __global__ void copy_tail_bytes(unsigned char *dst, const unsigned char *src, si
   for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
-__global__ void set_state_kernel(int *sel, unsigned long long *version, int idx, int s,
+__global__ void set_state_kernel(int *sel, unsigned long long *version, int *mfail, int idx, int s,
                                  unsigned long long v) {
   sel[idx] = s;
   version[idx] = v;
+  mfail[idx] = 0;
 }
 
 }  // namespace
@@ -79,9 +111,9 @@ cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s
   return cudaGetLastError();
 }
 
-cudaError_t launch_set_state(int *sel, unsigned long long *version, int idx, int sel_v,
+cudaError_t launch_set_state(int *sel, unsigned long long *version, int *mfail, int idx, int sel_v,
                              unsigned long long ver, cudaStream_t s) {
-  set_state_kernel<<<1, 1, 0, s>>>(sel, version, idx, sel_v, ver);
+  set_state_kernel<<<1, 1, 0, s>>>(sel, version, mfail, idx, sel_v, ver);
   count_launch();
   return cudaGetLastError();
 }

@@ -12,7 +12,7 @@
 //                    group's rows are the M dimension, W_down is read once per group);
 //   lr_finish_kernel y_b = Y32_b + Bᵀ u_b (+ residual), bf16, scattered through μ.
 // WRITE is one CTA per member: chunk mean m from the tail, w = A m, A' = A + η w mᵀ,
-// B copied; a non-finite candidate raises the group fail flag.
+// B copied; a non-finite candidate raises its owner's device fail flag.
 #include <cuda_bf16.h>
 
 #include <cstdlib>
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(512) lr_write_kernel(const LowRankWrite p) {
   }
   const int nb = R * dm / 8;                                  // B' = B
   for (int e = threadIdx.x; e < nb; e += blockDim.x) d4[R * nvec + e] = s4[R * nvec + e];
-  if (bad) atomicOr(p.fail_flag, 1);
+  if (bad) atomicOr(p.mfail + o, 1);        // per-member flag: the commit resolves members
 }
 
 __global__ void __launch_bounds__(256) lr_gather_kernel(const LowRankRead p) {

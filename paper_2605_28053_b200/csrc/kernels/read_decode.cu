@@ -297,6 +297,10 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
 #pragma unroll
         for (int r = 0; r < kMaxReadMembers; ++r) acc[r] = E::zero();
         if (lane == 0) p.Pdelta[(size_t)(m - 1) * dm + i] = s;
+        if (FUSE) {                                // per-member device failure flag (device-side App. H)
+          if (Upd<T>::bad(expmax)) atomicOr(p.mfail + p.owner_idx[m - 1], 1);
+          expmax = 0;
+        }
       }
       __syncwarp();
       int old = 0;
@@ -322,7 +326,6 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
     row = nrow;
     t = nt;
   }
-  if (FUSE && Upd<T>::bad(expmax)) atomicOr(p.fail_flag, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -575,6 +578,10 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
     if (lane == 0) p.Pdelta[(size_t)m * dm + i] = sum;
+    if (FUSE) {                                  // per-member device failure flag (device-side App. H)
+      if (Upd<__nv_bfloat16>::bad(expmax)) atomicOr(p.mfail + p.owner_idx[m], 1);
+      expmax = 0;
+    }
     __syncwarp();
     int old = 0;
     if (lane == 0) {
@@ -587,7 +594,6 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
       combine(i);
     }
   }
-  if (FUSE && Upd<__nv_bfloat16>::bad(expmax)) atomicOr(p.fail_flag, 1);
 }
 
 size_t smem_bytes(int n, int d_ff, int esize) { return (size_t)n * d_ff * esize; }

@@ -7,7 +7,7 @@
 //     ΔW̃_{v+1}[i][j] = ΔW_v[i][j] + η · Σ_{t<C} V_c[t][i] · Z_c[t][j].
 // The candidate goes to the owner's shadow slot (2·o + 1 − sel[o]); the
 // committed slot (2·o + sel[o]) is only read.  A non-finite candidate
-// element raises the group's device fail flag ("finite entries").
+// element raises its owner's device fail flag ("finite entries").
 //
 // This kernel is the true-fp32 path for σ.dtype = fp32 (BJ configs[0]
 // tolerance 1e-5 excludes tf32) and the fallback-free reference
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(NT) write_simt_kernel(const WriteParams p) {
       D[off] = st;
     }
   }
-  if (bad) atomicOr(p.fail_flag, 1);
+  if (bad) atomicOr(p.mfail + o, 1);        // per-member flag: the commit resolves members
 }
 
 }  // namespace

@@ -25,8 +25,9 @@
 //    store to the shadow slot; two TMEM accumulators overlap MMA(t+1) with
 //    epilogue(t);
 //  * the committed slot 2o+sel[o] is read and the shadow slot 2o+1−sel[o]
-//    written (device active-slot table); a non-finite candidate raises the
-//    group fail flag and the commit kernel then publishes nothing.
+//    written (device active-slot table); a non-finite candidate raises its
+//    owner's device fail flag and the commit kernel refuses
+//    that member (control.cu: device-side App. H resolution).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -58,7 +59,7 @@ struct TcParams {
   int n, d_model, d_ff, C, L, layer;
   const int *sel;
   float eta;
-  int *fail_flag;
+  int *mfail;
   int owner_idx[kMaxGroup];
 };
 
@@ -340,10 +341,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (kb >= kST) mbar_arrive(s_empty + (kb - kST) % kSB);
         }
       }
+      // per-member non-finite guard: flag this tile's owner (the commit resolves members)
+      if ((expmax & 0x7f80u) == 0x7f80u || (expmax >> 16) == 0x7f80u) atomicOr(p.mfail + o, 1);
+      expmax = 0;
     }
-    const bool bad = (expmax & 0x7f80u) == 0x7f80u || (expmax >> 16) == 0x7f80u;
     if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    if (bad) atomicOr(p.fail_flag, 1);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -404,7 +406,7 @@ cudaError_t launch_write_tc(const WriteParams &wp, cudaStream_t s) {
   p.layer = (int)(wp.layer_off / ((long long)wp.d_model * wp.d_ff));
   p.sel = wp.sel;
   p.eta = wp.eta;
-  p.fail_flag = wp.fail_flag;
+  p.mfail = wp.mfail;
   for (int b = 0; b < wp.n; ++b) p.owner_idx[b] = wp.owner_idx[b];
   const size_t smem = smem_bytes(wp.C);
   static size_t configured = 0;

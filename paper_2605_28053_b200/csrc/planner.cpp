@@ -32,10 +32,8 @@ struct ttt_planner {
 
 namespace {
 
-thread_local std::string g_plan_err;
-
 ttt_status perr(ttt_status s, const char *m) {
-  g_plan_err = m;
+  ttt::set_last_error(std::string(tttstate_status_name(s)) + ": " + m);   // tttstate_last_error()
   return s;
 }
 
@@ -56,6 +54,15 @@ bool older(const ttt_event &a, const ttt_event &b) {
 }
 
 }  // namespace
+
+namespace ttt {
+
+void planner_pending_owners(const ttt_planner *pl, std::unordered_set<uint64_t> &out) {
+  for (auto &kv : pl->buckets)
+    for (auto &e : kv.second) out.insert(e.owner);
+}
+
+}  // namespace ttt
 
 extern "C" {
 

@@ -3,6 +3,7 @@
 #include <cstdint>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/tttstate.h"
@@ -26,14 +27,18 @@ struct OwnerRec {
   uint64_t ckpt_v = 0;
   int ckpt_sel = 0;           // pinned pair slot (when ckpt_pool < 0)
   int ckpt_pool = -1;         // checkpoint-pool slot index (>= 0 when evicted)
+  uint64_t pending_seq = 0;   // latest write_commit of this owner not yet confirmed (0: confirmed)
 };
 
 struct Layout {
-  size_t slots = 0, tailZ = 0, tailV = 0, sel = 0, ver = 0, flags = 0, P = 0, tickets = 0;
+  size_t slots = 0, tailZ = 0, tailV = 0, sel = 0, ver = 0, flags = 0, mfail = 0, rlog = 0, P = 0, tickets = 0;
   size_t Xg = 0, Y32 = 0, U = 0, Ctr = 0, total = 0;   // low-rank READ workspace
 };
 
 Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt);
+void planner_pending_owners(const ttt_planner *pl, std::unordered_set<uint64_t> &out);
+void set_last_error(const std::string &msg);
+constexpr int kEventRing = 64;   // commit events kept (a newer record of a slot is a later point on the stream)
 
 }  // namespace ttt
 
@@ -50,8 +55,16 @@ struct ttt_pool {
   ttt::Layout lay;
   std::unordered_map<uint64_t, ttt::OwnerRec> owners;
   std::vector<int> free_idx, free_ckpt;
-  int fail_seen = 0;
+  int fail_seen = 0;          // device fail_count already reported by tttstate_sync
+  int rlog_read = 0;          // refusal-log records already drained (tttstate_refusals)
   float eta = 0.01f;          // η used by the fused C = 1 path (tttstate_set_eta)
+  // lazy commit confirmation: write_commit advances the host mirror optimistically and records
+  // an event; the commit kernel writes each member's post-commit (version, sel, seq) into
+  // pinned device-mapped host memory, read back only when a call needs the confirmed state
+  uint64_t commit_seq = 0;
+  std::vector<cudaEvent_t> ev_ring;                 // event recorded after commit seq k: ev_ring[k % size]
+  ttt::HostOwnerState *hstate = nullptr;            // [max_owners], cudaHostAllocMapped (host view)
+  ttt::HostOwnerState *hstate_dev = nullptr;        // the same memory as the kernels address it
 
   // device pointers (valid when !host_only)
   unsigned char *slot_ptr(long long slot) const {
@@ -60,6 +73,8 @@ struct ttt_pool {
   size_t slot_bytes() const { return (size_t)slot_elems * esize; }
   int *d_sel() const { return reinterpret_cast<int *>(arena + lay.sel); }
   unsigned long long *d_ver() const { return reinterpret_cast<unsigned long long *>(arena + lay.ver); }
-  int *d_fail_flag() const { return reinterpret_cast<int *>(arena + lay.flags); }
-  int *d_fail_count() const { return reinterpret_cast<int *>(arena + lay.flags + 16); }
+  int *d_fail_count() const { return reinterpret_cast<int *>(arena + lay.flags); }
+  int *d_rlog_count() const { return reinterpret_cast<int *>(arena + lay.flags + 16); }
+  int *d_mfail() const { return reinterpret_cast<int *>(arena + lay.mfail); }
+  ttt::RefusalRec *d_rlog() const { return reinterpret_cast<ttt::RefusalRec *>(arena + lay.rlog); }
 };

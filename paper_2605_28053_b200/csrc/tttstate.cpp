@@ -49,6 +49,8 @@ int device_sm_count() {
   return cached;
 }
 
+void set_last_error(const std::string &msg) { g_last_error = msg; }
+
 static ttt_status fail(ttt_status s, const std::string &msg) {
   g_last_error = std::string(tttstate_status_name(s)) + ": " + msg;
   return s;
@@ -81,7 +83,9 @@ Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt) {
   L.tailV = off;   off = align_up(off + (size_t)max_owners * s.n_layers * s.chunk * s.d_model * es, 1024);
   L.sel = off;     off = align_up(off + (size_t)max_owners * 4, 256);
   L.ver = off;     off = align_up(off + (size_t)max_owners * 8, 256);
-  L.flags = off;   off = align_up(off + 64, 256);
+  L.flags = off;   off = align_up(off + 64, 256);                  // fail_count, refusal-log counter
+  L.mfail = off;   off = align_up(off + (size_t)max_owners * 4, 256);  // per-owner device-failure flags
+  L.rlog = off;    off = align_up(off + (size_t)kRefusalLog * sizeof(RefusalRec), 256);
   // READ partials: base K-chunk slabs [kc][8][d_model] (kc ≤ ⌈d_ff/512⌉) + ΔW [8][d_model]
   L.P = off;       off = align_up(off + ((size_t)(s.d_ff + 511) / 512 + 1) * kMaxReadMembers * s.d_model * 4, 256);
   L.tickets = off; off = align_up(off + (size_t)s.d_model * 4, 1024);
@@ -156,6 +160,32 @@ void clear_applied(OwnerRec &r) {
 // A pinned checkpoint in the shadow slot must move to the checkpoint pool
 // before a WRITE overwrites the shadow (K5 checkpoint write).
 bool pinned_in_shadow(const OwnerRec &r) { return r.has_ckpt && r.ckpt_pool < 0 && r.ckpt_sel == 1 - r.sel; }
+
+void release_device(ttt_pool *p) {
+  for (cudaEvent_t e : p->ev_ring)
+    if (e) cudaEventDestroy(e);
+  p->ev_ring.clear();
+  if (p->hstate) cudaFreeHost(p->hstate);
+  p->hstate = p->hstate_dev = nullptr;
+}
+
+// Lazy confirmation of an owner's latest write_commit (the host mirror advanced optimistically):
+// wait for that commit's event — normally long complete — and take the device's outcome from the
+// mapped host record.  A member the device refused (non-finite candidate, control.cu) returns to
+// the version and slot it kept.  Called by every entry point that relies on the host's
+// (version, sel) of this owner: snapshot, rollback, fork, free, version, and WRITE paths that may
+// evict a pinned checkpoint.
+ttt_status confirm(ttt_pool *p, OwnerRec &r) {
+  if (!r.pending_seq) return TTT_OK;
+  CUDA_TRY(cudaEventSynchronize(p->ev_ring[r.pending_seq % p->ev_ring.size()]));
+  const volatile HostOwnerState *h = p->hstate + r.idx;
+  if (h->seq != r.pending_seq)
+    return fail(TTT_E_CUDA, "commit outcome record missing for seq " + std::to_string(r.pending_seq));
+  r.version = h->version;
+  r.sel = h->sel;
+  r.pending_seq = 0;
+  return TTT_OK;
+}
 
 cudaError_t evict_pinned(ttt_pool *p, OwnerRec &r, cudaStream_t s) {
   const int c = p->free_ckpt.back();
@@ -246,7 +276,19 @@ ttt_status tttstate_pool_create(const ttt_shape *shape, int32_t shape_id, int32_
   if (!p->host_only) {
     cudaError_t e = cudaMemset(p->arena + lay.sel, 0, lay.total - lay.sel);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    // commit outcomes: pinned device-mapped host memory (24 B per owner; not device memory)
+    if (e == cudaSuccess)
+      e = cudaHostAlloc(reinterpret_cast<void **>(&p->hstate), (size_t)max_owners * sizeof(HostOwnerState),
+                        cudaHostAllocMapped);
+    if (e == cudaSuccess) {
+      std::memset(p->hstate, 0, (size_t)max_owners * sizeof(HostOwnerState));
+      e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&p->hstate_dev), p->hstate, 0);
+    }
+    p->ev_ring.assign(kEventRing, nullptr);
+    for (int k = 0; k < kEventRing && e == cudaSuccess; ++k)
+      e = cudaEventCreateWithFlags(&p->ev_ring[k], cudaEventDisableTiming);
     if (e != cudaSuccess) {
+      release_device(p);
       delete p;
       return cuda_fail(e, "pool tables init");
     }
@@ -258,6 +300,7 @@ ttt_status tttstate_pool_create(const ttt_shape *shape, int32_t shape_id, int32_
 
 ttt_status tttstate_pool_destroy(ttt_pool *pool) {
   if (pool && !pool->host_only && pool->sh.backend == TTT_LOW_RANK) g_live_lowrank_pools.fetch_sub(1);
+  if (pool) release_device(pool);
   delete pool;
   return TTT_OK;
 }
@@ -275,7 +318,7 @@ ttt_status tttstate_alloc(ttt_pool *p, uint64_t owner, const void *init, uint64_
       CUDA_TRY(cudaMemcpyAsync(p->slot_ptr(2LL * idx), init, p->slot_bytes(), cudaMemcpyDeviceToDevice, s));
     else
       CUDA_TRY(cudaMemsetAsync(p->slot_ptr(2LL * idx), 0, p->slot_bytes(), s));
-    CUDA_TRY(launch_set_state(p->d_sel(), p->d_ver(), idx, 0, v0, s));
+    CUDA_TRY(launch_set_state(p->d_sel(), p->d_ver(), p->d_mfail(), idx, 0, v0, s));
   }
   p->free_idx.pop_back();
   OwnerRec r;
@@ -328,6 +371,7 @@ ttt_status tttstate_version(ttt_pool *p, uint64_t owner, uint64_t *v_out) {
   OwnerRec *r;
   ttt_status st = find_owner(p, owner, &r);
   if (st != TTT_OK) return st;
+  if ((st = confirm(p, *r)) != TTT_OK) return st;
   *v_out = r->version;
   return TTT_OK;
 }
@@ -378,14 +422,15 @@ ttt_status validate_group(ttt_pool *p, const ttt_group *g, const uint64_t *expec
   return TTT_OK;
 }
 
-// ---------------------------------------------------------------- READ
-ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void *X, const int32_t *x_rows,
-                      const void *Vt, const int32_t *v_rows, void *Y, const int32_t *y_rows,
-                      const void *resid, void *stream) {
-  NvtxRange nvtx_("read_apply");
-  std::vector<OwnerRec *> recs;
-  ttt_status st = check_group(p, g, recs);
-  if (st != TTT_OK) return st;
+}  // extern "C"
+
+namespace {
+
+// read_apply after check_group (serve_step resolves the group once for all layers)
+ttt_status read_apply_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec *> &recs, int32_t layer,
+                           const void *X, const int32_t *x_rows, const void *Vt, const int32_t *v_rows, void *Y,
+                           const int32_t *y_rows, const void *resid, cudaStream_t s) {
+  ttt_status st;
   const ttt_shape &sh = p->sh;
   if (layer < 0 || layer >= sh.n_layers) return fail(TTT_E_SHAPE, "layer out of range");
   for (int b = 0; b < g->n; ++b) {
@@ -404,11 +449,14 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
                     g_write_impl.load() != 1;
   int need_evict = 0;
   if (fuse)
-    for (int b = 0; b < g->n; ++b) need_evict += (recs[b]->n_applied == 0 && pinned_in_shadow(*recs[b]));
+    for (int b = 0; b < g->n; ++b)
+      if (recs[b]->n_applied == 0 && recs[b]->has_ckpt) {   // pinned_in_shadow needs the confirmed slot
+        if ((st = confirm(p, *recs[b])) != TTT_OK) return st;
+        need_evict += pinned_in_shadow(*recs[b]);
+      }
   if (need_evict > (int)p->free_ckpt.size()) return fail(TTT_E_POOL_FULL, "no free checkpoint slot for a pinned snapshot");
   if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
   if (!X || !Vt || !Y) return fail(TTT_E_INVALID_ARG, "null X/Vt/Y");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (fuse)
     for (int b = 0; b < g->n; ++b)
       if (recs[b]->n_applied == 0 && pinned_in_shadow(*recs[b])) CUDA_TRY(evict_pinned(p, *recs[b], s));
@@ -491,7 +539,7 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
     rp.d_model = sh.d_model; rp.d_ff = sh.d_ff;
     rp.fuse = fuse ? 1 : 0;
     rp.eta = p->eta;
-    rp.fail_flag = p->d_fail_flag();
+    rp.mfail = p->d_mfail();
     for (int k = 0; k < rp.n; ++k) {
       const int b = b0 + k;
       rp.owner_idx[k] = recs[b]->idx;
@@ -511,6 +559,20 @@ ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void
   return TTT_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+ttt_status read_apply(ttt_pool *p, const ttt_group *g, int32_t layer, const void *X, const int32_t *x_rows,
+                      const void *Vt, const int32_t *v_rows, void *Y, const int32_t *y_rows,
+                      const void *resid, void *stream) {
+  NvtxRange nvtx_("read_apply");
+  std::vector<OwnerRec *> recs;
+  ttt_status st = check_group(p, g, recs);
+  if (st != TTT_OK) return st;
+  return read_apply_recs(p, g, recs, layer, X, x_rows, Vt, v_rows, Y, y_rows, resid, static_cast<cudaStream_t>(stream));
+}
+
 ttt_status tttstate_set_eta(ttt_pool *p, float eta) {
   if (!p) return fail(TTT_E_INVALID_ARG, "null pool");
   p->eta = eta;
@@ -522,9 +584,14 @@ ttt_status tttstate_step_done(ttt_pool *p, const ttt_group *g) {
   ttt_status st = check_group(p, g, recs);
   if (st != TTT_OK) return st;
   if (g->effect != TTT_READ) return fail(TTT_E_WRONG_EFFECT, "step_done is for READ groups (write_commit ends a WRITE step)");
-  for (int b = 0; b < g->n; ++b)
+  for (int b = 0; b < g->n; ++b) {
+    // a READ step ends below the boundary: an owner at C-1 (or one whose chunk was applied by
+    // read_apply_chunk) must end its step with write_commit
+    if (recs[b]->chunk_mode || recs[b]->tail_len >= p->sh.chunk - 1)
+      return fail(TTT_E_WRONG_EFFECT, "owner " + std::to_string(g->owner_map[b]) + " is at a chunk boundary (WRITE step)");
     if (recs[b]->n_applied != p->sh.n_layers)
       return fail(TTT_E_NOT_APPLIED, "owner " + std::to_string(g->owner_map[b]));
+  }
   for (int b = 0; b < g->n; ++b) {
     recs[b]->tail_len += 1;
     clear_applied(*recs[b]);
@@ -577,12 +644,13 @@ ttt_status read_apply_chunk(ttt_pool *p, const ttt_group *g, int32_t layer, cons
 }
 
 // ---------------------------------------------------------------- WRITE + commit
-ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32_t *fail_mask,
-                        uint64_t *new_versions, void *stream) {
-  NvtxRange nvtx_("write_commit");
-  std::vector<OwnerRec *> recs;
-  ttt_status st = check_group(p, g, recs);
-  if (st != TTT_OK) return st;
+}  // extern "C"
+
+namespace {
+
+ttt_status write_commit_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec *> &recs, float eta,
+                             const uint32_t *fail_mask, uint64_t *new_versions, cudaStream_t s) {
+  ttt_status st;
   const ttt_shape &sh = p->sh;
   if (g->effect != TTT_WRITE) return fail(TTT_E_WRONG_EFFECT, "write_commit needs a WRITE group");
   int need_evict = 0, n_fused = 0;
@@ -590,9 +658,13 @@ ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32
     OwnerRec &r = *recs[b];
     if (r.tail_len != sh.chunk - 1) return fail(TTT_E_TAIL_NOT_FULL, "owner " + std::to_string(g->owner_map[b]));
     if (r.n_applied != sh.n_layers) return fail(TTT_E_NOT_APPLIED, "owner " + std::to_string(g->owner_map[b]));
-    need_evict += pinned_in_shadow(r);
     n_fused += r.fused_layers == sh.n_layers;
   }
+  for (int b = 0; b < g->n; ++b)
+    if (recs[b]->has_ckpt) {                        // pinned_in_shadow needs the confirmed slot
+      if ((st = confirm(p, *recs[b])) != TTT_OK) return st;
+      need_evict += pinned_in_shadow(*recs[b]);
+    }
   const bool fused = n_fused == g->n;               // every candidate already written by read_apply (f3)
   if (n_fused != 0 && !fused) return fail(TTT_E_INVALID_ARG, "group mixes fused and unfused members");
   if (fused && eta != p->eta) return fail(TTT_E_INVALID_ARG, "eta differs from the pool's fused-path eta");
@@ -605,7 +677,6 @@ ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32
   if (fail_mask)
     for (int b = 0; b < g->n; ++b) forced |= (fail_mask[b / 32] >> (b % 32)) & 1u;
   if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!fused && sh.backend == TTT_LOW_RANK) {
     for (int b = 0; b < g->n; ++b)
       if (pinned_in_shadow(*recs[b])) CUDA_TRY(evict_pinned(p, *recs[b], s));
@@ -617,7 +688,7 @@ ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32
     lw.tailZ = p->arena + p->lay.tailZ;
     lw.tz_owner = p->tz_owner;
     lw.eta = eta;
-    lw.fail_flag = p->d_fail_flag();
+    lw.mfail = p->d_mfail();
     for (int b = 0; b < g->n; ++b) lw.owner_idx[b] = recs[b]->idx;
     for (int l = 0; l < sh.n_layers; ++l) {
       lw.layer_off = (long long)l * p->E;
@@ -636,7 +707,7 @@ ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32
     wp.tailV = p->arena + p->lay.tailV;
     wp.tz_owner = p->tz_owner; wp.tv_owner = p->tv_owner;
     wp.eta = eta;
-    wp.fail_flag = p->d_fail_flag();
+    wp.mfail = p->d_mfail();
     wp.n = g->n; wp.d_model = sh.d_model; wp.d_ff = sh.d_ff; wp.C = sh.chunk;
     wp.max_owners = p->max_owners; wp.max_slots = 2 * p->max_owners + p->n_ckpt;
     for (int b = 0; b < g->n; ++b) wp.owner_idx[b] = recs[b]->idx;
@@ -651,11 +722,18 @@ ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32
   CommitParams cp{};
   cp.sel = p->d_sel();
   cp.version = p->d_ver();
-  cp.fail_flag = p->d_fail_flag();
+  cp.mfail = p->d_mfail();
   cp.fail_count = p->d_fail_count();
+  cp.rlog_count = p->d_rlog_count();
+  cp.rlog = p->d_rlog();
+  cp.hstate = p->hstate_dev;
+  cp.seq = forced ? 0 : p->commit_seq + 1;
   cp.forced_fail = forced ? 1 : 0;
   cp.n = g->n;
-  for (int b = 0; b < g->n; ++b) cp.owner_idx[b] = recs[b]->idx;
+  for (int b = 0; b < g->n; ++b) {
+    cp.owner_idx[b] = recs[b]->idx;
+    cp.owner_id[b] = g->owner_map[b];
+  }
   const bool partial = forced && (g_test_hook.load() & TTT_HOOK_NO_GROUP_ATOMICITY);
   cp.partial = partial ? 1 : 0;
   if (partial)
@@ -671,14 +749,37 @@ ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32
       clear_applied(r);
     }
   if (forced) return fail(TTT_E_WRITE_FAILED, "injected failure: group not committed");
+  // optimistic host mirror: every member at v+1 unless the device refuses it (confirm())
+  const uint64_t seq = ++p->commit_seq;
+  CUDA_TRY(cudaEventRecord(p->ev_ring[seq % p->ev_ring.size()], s));
   for (int b = 0; b < g->n; ++b) {
     OwnerRec &r = *recs[b];
     r.sel ^= 1;
     r.version += 1;
     r.tail_len = 0;
+    r.pending_seq = seq;
     clear_applied(r);
     if (new_versions) new_versions[b] = r.version;
   }
+  return TTT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ttt_status write_commit(ttt_pool *p, const ttt_group *g, float eta, const uint32_t *fail_mask,
+                        uint64_t *new_versions, void *stream) {
+  NvtxRange nvtx_("write_commit");
+  std::vector<OwnerRec *> recs;
+  ttt_status st = check_group(p, g, recs);
+  if (st != TTT_OK) return st;
+  return write_commit_recs(p, g, recs, eta, fail_mask, new_versions, static_cast<cudaStream_t>(stream));
+}
+
+ttt_status tttstate_last_commit_seq(ttt_pool *p, uint64_t *seq_out) {
+  if (!p || !seq_out) return fail(TTT_E_INVALID_ARG, "null arg");
+  *seq_out = p->commit_seq;
   return TTT_OK;
 }
 
@@ -690,6 +791,7 @@ ttt_status tttstate_snapshot(ttt_pool *p, uint64_t owner, void *stream) {
   OwnerRec *r;
   ttt_status st = find_owner(p, owner, &r);
   if (st != TTT_OK) return st;
+  if ((st = confirm(p, *r)) != TTT_OK) return st;   // pin the committed (confirmed) slot only
   if (r->ckpt_pool >= 0) p->free_ckpt.push_back(r->ckpt_pool);
   r->has_ckpt = true;
   r->ckpt_v = r->version;
@@ -706,6 +808,7 @@ ttt_status rollback(ttt_pool *p, uint64_t owner, uint64_t *v_out, void *stream) 
   if (st != TTT_OK) return st;
   if (!r->has_ckpt) return fail(TTT_E_NO_CHECKPOINT, "owner " + std::to_string(owner));
   if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  if ((st = confirm(p, *r)) != TTT_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int new_sel;
   if (r->ckpt_pool < 0) {
@@ -715,7 +818,7 @@ ttt_status rollback(ttt_pool *p, uint64_t owner, uint64_t *v_out, void *stream) 
     CUDA_TRY(launch_copy(p->slot_ptr(2LL * r->idx + new_sel), p->slot_ptr(2LL * p->max_owners + r->ckpt_pool),
                          p->slot_bytes(), s));
   }
-  CUDA_TRY(launch_set_state(p->d_sel(), p->d_ver(), r->idx, new_sel, r->ckpt_v, s));
+  CUDA_TRY(launch_set_state(p->d_sel(), p->d_ver(), p->d_mfail(), r->idx, new_sel, r->ckpt_v, s));
   r->sel = new_sel;
   r->version = r->ckpt_v;
   r->tail_len = 0;
@@ -733,10 +836,11 @@ ttt_status tttstate_fork(ttt_pool *p, uint64_t src, uint64_t dst, void *stream) 
   if (p->owners.count(dst)) return fail(TTT_E_DUPLICATE_OWNER, "owner " + std::to_string(dst));
   if (p->free_idx.empty()) return fail(TTT_E_POOL_FULL, "no free owner slot");
   if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  if ((st = confirm(p, *rs)) != TTT_OK) return st;   // copy the committed (confirmed) slot
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int idx = p->free_idx.back();
   CUDA_TRY(launch_copy(p->slot_ptr(2LL * idx), p->slot_ptr(2LL * rs->idx + rs->sel), p->slot_bytes(), s));
-  CUDA_TRY(launch_set_state(p->d_sel(), p->d_ver(), idx, 0, rs->version, s));
+  CUDA_TRY(launch_set_state(p->d_sel(), p->d_ver(), p->d_mfail(), idx, 0, rs->version, s));
   p->free_idx.pop_back();
   OwnerRec r;
   r.idx = idx;
@@ -752,27 +856,150 @@ ttt_status tttstate_sync(ttt_pool *p, void *stream, int32_t *n_failed_out) {
   if (n_failed_out) *n_failed_out = 0;
   if (p->host_only) return TTT_OK;
   CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  for (auto &kv : p->owners) {                       // every pending commit is complete now
+    ttt_status st = confirm(p, kv.second);
+    if (st != TTT_OK) return st;
+  }
   int count = 0;
   CUDA_TRY(cudaMemcpy(&count, p->d_fail_count(), sizeof(int), cudaMemcpyDeviceToHost));
   if (count == p->fail_seen) return TTT_OK;
   const int nf = count - p->fail_seen;
   p->fail_seen = count;
-  std::vector<int> sel(p->max_owners);
-  std::vector<unsigned long long> ver(p->max_owners);
-  CUDA_TRY(cudaMemcpy(sel.data(), p->d_sel(), sel.size() * 4, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(ver.data(), p->d_ver(), ver.size() * 8, cudaMemcpyDeviceToHost));
-  for (auto &kv : p->owners) {
-    OwnerRec &r = kv.second;
-    if (r.version != ver[r.idx] || r.sel != sel[r.idx]) {   // assumed committed, device refused
-      r.version = ver[r.idx];
-      r.sel = sel[r.idx];
-      r.tail_len = p->sh.chunk - 1;                           // tail retained for the retry
-      std::fill(r.applied.begin(), r.applied.end(), 1);
-      r.n_applied = p->sh.n_layers;
-    }
-  }
   if (n_failed_out) *n_failed_out = nf;
-  return fail(TTT_E_WRITE_FAILED, std::to_string(nf) + " group(s) failed on the device");
+  return fail(TTT_E_WRITE_FAILED, std::to_string(nf) + " group(s) had members refused on the device");
+}
+
+ttt_status tttstate_refusals(ttt_pool *p, uint64_t *owners, uint64_t *versions, uint64_t *seqs, int32_t cap,
+                             int32_t *n_out, void *stream) {
+  if (!p || !n_out || cap < 0 || (cap > 0 && (!owners || !versions || !seqs))) return fail(TTT_E_INVALID_ARG, "null arg");
+  *n_out = 0;
+  if (p->host_only) return TTT_OK;
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  int count = 0;
+  CUDA_TRY(cudaMemcpy(&count, p->d_rlog_count(), sizeof(int), cudaMemcpyDeviceToHost));
+  const int avail = count - p->rlog_read;
+  if (avail > kRefusalLog) return fail(TTT_E_CAPACITY, "refusal log overflowed (drain more often)");
+  const int n = std::min(avail, cap);
+  std::vector<RefusalRec> recs(n);
+  for (int k = 0; k < n; ++k)
+    CUDA_TRY(cudaMemcpy(&recs[k], p->d_rlog() + (p->rlog_read + k) % kRefusalLog, sizeof(RefusalRec),
+                        cudaMemcpyDeviceToHost));
+  for (int k = 0; k < n; ++k) {
+    owners[k] = recs[k].owner;
+    versions[k] = recs[k].version;
+    seqs[k] = recs[k].seq;
+  }
+  p->rlog_read += n;
+  *n_out = n;
+  return TTT_OK;
+}
+
+// ---------------------------------------------------------------- one serving-loop iteration
+ttt_status tttstate_serve_step(ttt_pool *p, ttt_planner *pl, const uint64_t *owners, int32_t n, int64_t clock,
+                               const ttt_step_io *io, float eta, const uint64_t *fail_owners, int32_t n_fail,
+                               ttt_step_out *out, void *stream) {
+  NvtxRange nvtx_("tttstate_serve_step");
+  if (!p || !pl || !io || !out || n < 0 || (n > 0 && !owners) || n_fail < 0 || (n_fail > 0 && !fail_owners))
+    return fail(TTT_E_INVALID_ARG, "null arg / negative count");
+  if (!out->groups || !out->owner_buf || out->group_cap < 0 || out->owner_cap < 0)
+    return fail(TTT_E_INVALID_ARG, "null output buffers");
+  out->n_groups = out->n_rejected = out->n_read = out->n_write = out->n_injected = 0;
+  if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  if (!io->X || !io->Vt || !io->Y) return fail(TTT_E_INVALID_ARG, "null X/Vt/Y");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // owner -> token row; validate every owner before any side effect
+  std::unordered_map<uint64_t, int32_t> row;
+  row.reserve(2 * (size_t)n + 1);
+  for (int i = 0; i < n; ++i) {
+    OwnerRec *r;
+    ttt_status st = find_owner(p, owners[i], &r);
+    if (st != TTT_OK) return st;
+    if (!row.emplace(owners[i], io->rows ? io->rows[i] : i).second)
+      return fail(TTT_E_OWNER_COLLISION, "owner " + std::to_string(owners[i]) + " listed twice");
+  }
+  // a1 NextStep: an event for every listed owner without one pending in the planner
+  std::unordered_set<uint64_t> pend;
+  planner_pending_owners(pl, pend);
+  std::vector<ttt_event> ev;
+  ev.reserve(n);
+  for (int i = 0; i < n; ++i)
+    if (!pend.count(owners[i])) {
+      ev.emplace_back();
+      tttstate_next_event(p, owners[i], clock, &ev.back());
+    }
+  // a2 LegalGroups (no side effect on error)
+  int32_t n_groups = 0, n_rej = 0;
+  ttt_status st = plan_batch(pl, ev.data(), (int32_t)ev.size(), clock, out->groups, out->group_cap, out->owner_buf,
+                             out->owner_cap, &n_groups, out->rejected, out->rej_cap, &n_rej);
+  if (st != TTT_OK) return st;
+  out->n_groups = n_groups;
+  out->n_rejected = n_rej;
+  std::unordered_set<uint64_t> failing(fail_owners, fail_owners + n_fail);
+  const size_t es = p->esize;
+  std::vector<OwnerRec *> recs, one;
+  std::vector<int32_t> rows;
+  size_t off = 0;
+  for (int k = 0; k < n_groups; ++k) {
+    const ttt_group &g = out->groups[k];
+    if ((st = check_group(p, &g, recs)) != TTT_OK) return st;
+    if (out->injected) out->injected[k] = 0;
+    rows.resize(g.n);
+    for (int b = 0; b < g.n; ++b) {
+      auto it = row.find(g.owner_map[b]);
+      if (it == row.end()) return fail(TTT_E_UNKNOWN_OWNER, "planner issued an owner outside this step");
+      rows[b] = it->second;
+      if (out->v_before) out->v_before[off + b] = recs[b]->version;
+      if (out->member_seq) out->member_seq[off + b] = 0;
+    }
+    for (int l = 0; l < p->sh.n_layers; ++l) {    // a3 + a4: one dependent READ launch per layer
+      const unsigned char *X = static_cast<const unsigned char *>(io->X) + (size_t)l * io->x_layer_stride * es;
+      const unsigned char *V = static_cast<const unsigned char *>(io->Vt) + (size_t)l * io->v_layer_stride * es;
+      unsigned char *Y = static_cast<unsigned char *>(io->Y) + (size_t)l * io->y_layer_stride * es;
+      const unsigned char *R = io->resid ? static_cast<const unsigned char *>(io->resid) + (size_t)l * io->r_layer_stride * es
+                                         : nullptr;
+      if ((st = read_apply_recs(p, &g, recs, l, X, rows.data(), V, rows.data(), Y, rows.data(), R, s)) != TTT_OK)
+        return st;
+    }
+    if (g.effect == TTT_READ) {                    // UpdateKVAndTailMetadata
+      for (int b = 0; b < g.n; ++b) {
+        recs[b]->tail_len += 1;
+        clear_applied(*recs[b]);
+      }
+      out->n_read += g.n;
+    } else {                                       // a5 + a6 (+ App. H fallback on an injected failure)
+      std::vector<uint32_t> mask((g.n + 31) / 32, 0u);
+      bool any = false;
+      for (int b = 0; b < g.n; ++b)
+        if (failing.count(g.owner_map[b])) {
+          mask[b / 32] |= 1u << (b % 32);
+          any = true;
+        }
+      const bool prof = io->ev_write_begin && io->ev_write_end && out->n_write == 0;
+      if (prof) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(io->ev_write_begin), s));
+      st = write_commit_recs(p, &g, recs, eta, any ? mask.data() : nullptr, nullptr, s);
+      if (prof && st == TTT_OK) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(io->ev_write_end), s));
+      if (st == TTT_OK) {
+        for (int b = 0; b < g.n; ++b)
+          if (out->member_seq) out->member_seq[off + b] = p->commit_seq;
+      } else if (st == TTT_E_WRITE_FAILED && any) {
+        if (out->injected) out->injected[k] = 1;
+        out->n_injected += 1;
+        for (int b = 0; b < g.n; ++b) {            // serial singletons in μ order
+          ttt_group g1 = g;
+          g1.n = 1;
+          g1.owner_map = g.owner_map + b;
+          one.assign(1, recs[b]);
+          if ((st = write_commit_recs(p, &g1, one, eta, nullptr, nullptr, s)) != TTT_OK) return st;
+          if (out->member_seq) out->member_seq[off + b] = p->commit_seq;
+        }
+      } else {
+        return st;
+      }
+      out->n_write += g.n;
+    }
+    off += g.n;
+  }
+  return TTT_OK;
 }
 
 // ---------------------------------------------------------------- test hooks

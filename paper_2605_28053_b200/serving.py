@@ -3,18 +3,26 @@
     View -> NextStep -> LegalGroups -> ExecuteOperatorGroup -> ReturnOutputs
          -> CommitVersions (WRITE) -> UpdateKVAndTailMetadata
 
-Python here only sequences calls into libtttstate.so: event extraction
-(tttstate_next_event), planning (plan_batch), READ (read_apply), WRITE +
-commit (write_commit), control (snapshot / rollback) all run natively.  A
-WRITE group that fails is re-run as serial singletons in μ order (App. H
-fallback handling).  PyTorch provides the device arena and
-streams only.
+Python here only sequences calls into libtttstate.so.  The default step is ONE
+native call per decode step, `tttstate_serve_step` (NextStep -> plan_batch ->
+L read_apply launches per group -> step done / write_commit, with the App. H
+singleton retry of a group that hits an injected failure), so the host cost
+per step does not grow with the layer count and nothing waits for the GPU.
+Controls (snapshot / rollback / fork / release) are issued before the step.
+`step_percall()` sequences the same operators with one C-ABI call per
+operator (the stress suite uses it to inspect state between calls).
+
+Commits are provisional until confirmed (include/tttstate.h "Commit
+confirmation"): the device refuses a member whose candidate is not finite and
+resolves App. H's singleton retries itself.  `finish()` (or `drain()`)
+synchronises, reads the device refusal records and writes the final commit log:
+a group with a refused member is logged as failed, then each member's singleton
+outcome.  PyTorch provides the device arena and streams only.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
-
 import time
+from dataclasses import dataclass, field
 
 import torch
 
@@ -36,6 +44,7 @@ class Engine:
         self.eta = float(torch.tensor(eta, dtype=torch.float32))
         self.shape = capi.make_shape(d_model, d_ff, chunk, n_layers, dtype, backend=backend, rank=rank)
         self.backend, self.rank = backend, rank
+        self.max_owners = max_owners
         self.arena_bytes = capi.tttstate_pool_bytes(self.shape, max_owners, n_ckpt)
         self._arena = torch.empty(self.arena_bytes + 1024, dtype=torch.uint8, device=device)
         base = (self._arena.data_ptr() + 1023) // 1024 * 1024
@@ -69,8 +78,22 @@ class RunLog:
     plan: list = field(default_factory=list)        # (issue_step, effect, [streams], [ready])
     versions: dict = field(default_factory=dict)
     fallbacks: int = 0
-    device_failures: int = 0
+    device_failures: int = 0                        # groups with a member refused on the device
+    rejected: int = 0                               # planner rejections (re-extracted next step)
     branches: dict = field(default_factory=dict)    # live branch owner -> version
+
+
+@dataclass
+class StepIO:
+    """One decode step's device operands: layer l of X / Vt / Y starts *_stride elements after
+    layer l-1; the token of the i-th listed stream sits at row rows[i] of every layer."""
+    X: torch.Tensor
+    x_stride: int
+    Vt: torch.Tensor
+    v_stride: int
+    Y: torch.Tensor
+    y_stride: int
+    rows: list
 
 
 class InputSource:
@@ -82,6 +105,14 @@ class InputSource:
     def tail_prefill(self, s: int):               # (n, Z [L,n,d_ff], V [L,n,d_model]) or None
         return None
 
+    def step_io(self, streams, positions) -> StepIO:
+        """Operands of one native step for the listed (stream, position) tokens."""
+        raise NotImplementedError
+
+    def on_step(self, executed, io: StepIO):
+        """executed: [(s, p, row)] tokens the step ran (ReturnOutputs); their y is in io.Y."""
+
+    # per-operator path (Server.step_percall)
     def group_io(self, l: int, streams, positions):
         """-> (X, x_rows, Vt, v_rows, Y, y_rows) device tensors (+ row maps or None)."""
         raise NotImplementedError
@@ -93,15 +124,16 @@ class InputSource:
 class Server:
     """Alg. 1 state for one trace: per-stream position, pending events, logs.
 
-    `step()` runs exactly one iteration of the serving loop at the current
-    clock.  With `profile=True` every read_apply / write_commit is bracketed by
-    CUDA events on `stream` (used by bench.py for the live per-kernel roofline).
+    `step()` runs exactly one iteration of the serving loop at the current clock
+    (one native call).  With `profile=True` CUDA events on `stream` bracket every
+    `profile_every`-th READ-only step (read_events: (start, end, READ launches))
+    and every step's first WRITE (write_events), for bench.py's live rooflines.
     """
 
-    def __init__(self, eng: Engine, tr, src: InputSource, stream=None, sync_writes: bool = True,
-                 profile: bool = False, profile_every: int = 1):
+    def __init__(self, eng: Engine, tr, src: InputSource, stream=None, profile: bool = False,
+                 profile_every: int = 1, native: bool = True):
         self.eng, self.tr, self.src, self.stream = eng, tr, src, stream
-        self.sync_writes, self.profile, self.profile_every = sync_writes, profile, max(1, profile_every)
+        self.profile, self.profile_every, self.native = profile, max(1, profile_every), native
         self.log = RunLog()
         self.owners = [tr.owner(s) for s in range(tr.n_streams)]
         self.by_owner = {o: s for s, o in enumerate(self.owners)}
@@ -113,8 +145,26 @@ class Server:
         self.branches: set = set()
         self.clock = 0
         self.read_events: list = []       # (start, end, launches): events around a step's back-to-back READs
-        self.write_events: list = []      # (start, end) around write_commit
-        self.plan_s = 0.0                 # host seconds in NextStep + LegalGroups (P:525's overhead)
+        self.write_events: list = []      # (start, end) around the step's first write_commit
+        self.plan_s = 0.0                 # host seconds in View/controls + marshalling (P:525's overhead share)
+        self._items: list = []            # commit log items, expanded by drain() (provisional commits)
+        self._has_controls = bool(tr.controls)
+        self.bufs = capi.StepBuffers(eng.max_owners)
+        self._wev = self._fresh_pair() if profile else (None, None)
+
+    def _stream_obj(self):
+        return torch.cuda.current_stream() if self.stream is None else self.stream
+
+    def _fresh_pair(self):
+        pair = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        for e in pair:                    # materialise the cudaEvent_t the library records into
+            e.record(self._stream_obj())
+        return pair
+
+    def _ev(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(self._stream_obj())
+        return e
 
     def admit(self):
         eng, tr, src = self.eng, self.tr, self.src
@@ -127,12 +177,100 @@ class Server:
     def done(self) -> bool:
         return all(p >= self.tr.n_steps for p in self.pos)
 
-    def _ev(self):
-        e = torch.cuda.Event(enable_timing=True)
-        e.record(torch.cuda.current_stream() if self.stream is None else self.stream)
-        return e
+    # ---------------------------------------------------------------- View + controls
+    def _controls(self, s):
+        pool, stream, log, tr = self.eng.pool, self.stream, self.log, self.tr
+        o = self.owners[s]
+        for op in tr.controls_at(s, self.pos[s]):
+            if op == "snapshot":
+                capi.tttstate_snapshot(pool, o, stream)
+            elif op == "rollback":
+                vb = capi.tttstate_version(pool, o)
+                va = capi.rollback(pool, o, stream)
+                self._items.append((s, self.pos[s], vb, va, "rolled_back"))
+            elif op == "fork":                                  # new lineage
+                k = self.forks.get(s, 0)
+                capi.tttstate_fork(pool, o, tr.branch_owner(s, k), stream)
+                self.branches.add(tr.branch_owner(s, k))
+                self.forks[s] = k + 1
+            elif op == "release":
+                b = tr.branch_owner(s, self.forks[s] - 1)
+                capi.tttstate_free(pool, b)
+                self.branches.discard(b)
+
+    def _injected(self, s) -> bool:
+        p = self.pos[s]
+        return self._has_controls and "fail" in self.tr.controls_at(s, p) and (s, p) not in self.failed_once
 
     def step(self):
+        if not self.native:
+            return self.step_percall()
+        eng, tr, src, log, bufs = self.eng, self.tr, self.src, self.log, self.bufs
+        clock = self.clock
+        t0 = time.perf_counter()
+        active = [s for s in range(tr.n_streams) if self.pos[s] < tr.n_steps]
+        n_fail = 0
+        for s in active:
+            if s not in self.pending:
+                if self._has_controls:
+                    self._controls(s)
+                self.ready_at[s] = clock
+            if self._injected(s):
+                bufs.fail[n_fail] = self.owners[s]
+                n_fail += 1
+        io = src.step_io(active, [self.pos[s] for s in active])
+        for i, s in enumerate(active):
+            bufs.owners[i] = self.owners[s]
+            bufs.rows[i] = io.rows[i]
+        prof = self.profile and clock % self.profile_every == 0
+        if prof:
+            e0 = self._ev()
+        self.plan_s += time.perf_counter() - t0
+        out = capi.tttstate_serve_step(eng.pool, eng.planner, bufs, len(active), clock, io.X, io.x_stride, io.Vt,
+                                       io.v_stride, io.Y, io.y_stride, tr.eta, n_fail, stream=self.stream,
+                                       ev_write=self._wev)
+        t1 = time.perf_counter()
+        for s in active:
+            self.pending.add(s)
+        for k in range(out.n_rejected):                          # stale pending events: re-extract
+            self.pending.discard(self.by_owner[bufs.rejected[k].owner])
+            log.rejected += 1
+        executed = []
+        n_read_launches = 0
+        row_of = {s: io.rows[i] for i, s in enumerate(active)}
+        for eff, owners, vb, seqs, inj in bufs.groups_issued():
+            ss = [self.by_owner[o] for o in owners]
+            ps = [self.pos[s] for s in ss]
+            log.plan.append((clock, eff, ss, [self.ready_at[s] for s in ss]))
+            log.census[eff] += len(ss)
+            if eff == READ:
+                n_read_launches += (len(ss) + 7) // 8
+            else:
+                if inj:
+                    for s, p, v in zip(ss, ps, vb):
+                        self.failed_once.add((s, p))
+                        self._items.append((s, p, v, v, "failed"))
+                    log.fallbacks += 1
+                    for o, s, p, v, q in zip(owners, ss, ps, vb, seqs):   # singleton retries
+                        self._items.append(("single", q, o, s, p, v))
+                else:
+                    self._items.append(("group", seqs[0], list(zip(owners, ss, ps, vb))))
+            for s in ss:
+                executed.append((s, self.pos[s], row_of[s]))
+                self.pos[s] += 1
+                self.pending.discard(s)
+        src.on_step(executed, io)
+        if self.profile:
+            if out.n_write:
+                self.write_events.append(self._wev)
+                self._wev = self._fresh_pair()
+            elif prof and n_read_launches:
+                self.read_events.append((e0, self._ev(), n_read_launches * tr.n_layers))
+        self.plan_s += time.perf_counter() - t1
+        self.clock += 1
+
+    # ---------------------------------------------------------------- per-operator path
+    def step_percall(self):
         eng, tr, src, log, stream = self.eng, self.tr, self.src, self.log, self.stream
         pool, owners, clock = eng.pool, self.owners, self.clock
         t_plan = time.perf_counter()
@@ -140,87 +278,82 @@ class Server:
         for s in range(tr.n_streams):                                   # View + controls
             if self.pos[s] < tr.n_steps and s not in self.pending:
                 ready.append(s)
-                for op in tr.controls_at(s, self.pos[s]):
-                    if op == "snapshot":
-                        capi.tttstate_snapshot(pool, owners[s], stream)
-                    elif op == "rollback":
-                        vb = capi.tttstate_version(pool, owners[s])
-                        va = capi.rollback(pool, owners[s], stream)
-                        log.commits.append((s, self.pos[s], vb, va, "rolled_back"))
-                    elif op == "fork":                                  # new lineage
-                        k = self.forks.get(s, 0)
-                        capi.tttstate_fork(pool, owners[s], tr.branch_owner(s, k), stream)
-                        self.branches.add(tr.branch_owner(s, k))
-                        self.forks[s] = k + 1
-                    elif op == "release":
-                        b = tr.branch_owner(s, self.forks[s] - 1)
-                        capi.tttstate_free(pool, b)
-                        self.branches.discard(b)
-        # NextStep for every ready stream in one call
+                self._controls(s)
         events = capi.tttstate_next_events(pool, [owners[s] for s in ready], clock) if ready else []
         for s in ready:
             self.pending.add(s)
             self.ready_at[s] = clock
         groups, rejected = capi.plan_batch(eng.planner, events, clock)  # LegalGroups
         self.plan_s += time.perf_counter() - t_plan
-        if rejected:
-            raise RuntimeError(f"planner rejected events of a well-formed trace: {rejected}")
+        for r in rejected:
+            self.pending.discard(self.by_owner[r.owner])
+            log.rejected += 1
         for g in groups:
             ss = [self.by_owner[o] for o in g.owners]
             ps = [self.pos[s] for s in ss]
             log.plan.append((g.issue_step, g.effect, ss, [self.ready_at[s] for s in ss]))
-            prof = self.profile and clock % self.profile_every == 0
-            if prof:                    # one event pair per group: per-launch events would break PDL overlap
-                e0 = self._ev()
             for l in range(tr.n_layers):                                # ExecuteOperatorGroup
                 X, xr, Vt, vr, Y, yr = src.group_io(l, ss, ps)
                 capi.read_apply(pool, g, l, X, xr, Vt, vr, Y, yr, None, stream)
                 src.on_output(l, ss, ps, Y, yr)                         # ReturnOutputs
-            if prof:
-                self.read_events.append((e0, self._ev(), tr.n_layers))
             log.census[g.effect] += len(ss)
             if g.effect == READ:
                 capi.tttstate_step_done(pool, g)                        # UpdateKVAndTailMetadata
             else:
-                self._write(g, ss, ps)
+                self._write_percall(g, ss, ps)
             for s in ss:
                 self.pos[s] += 1
                 self.pending.discard(s)
         self.clock += 1
 
-    def _write(self, g, ss, ps):
-        eng, tr, log, stream = self.eng, self.tr, self.log, self.stream
-        pool = eng.pool
+    def _write_percall(self, g, ss, ps):
+        tr, log, stream, pool = self.tr, self.log, self.stream, self.eng.pool
         vb = [capi.tttstate_version(pool, o) for o in g.owners]
-        mask = [("fail" in tr.controls_at(s, p)) and (s, p) not in self.failed_once for s, p in zip(ss, ps)]
+        mask = [self._injected(s) for s in ss]
         try:                                                            # CommitVersions
-            if self.profile:
-                e0 = self._ev()
             capi.write_commit(pool, g, tr.eta, mask if any(mask) else None, stream)
-            if self.profile:
-                self.write_events.append((e0, self._ev()))
-            ok = True
-            if self.sync_writes and capi.tttstate_sync(pool, stream):
-                log.device_failures += 1
-                ok = False
+            self._items.append(("group", capi.tttstate_last_commit_seq(pool), list(zip(g.owners, ss, ps, vb))))
+            return
         except TTTError as e:
             if e.status != capi.TTT_E_WRITE_FAILED:
                 raise
-            ok = False
-        if ok:
-            for s, p, v in zip(ss, ps, vb):
-                log.commits.append((s, p, v, v + 1, "ok"))
-            return
         for s, p, v in zip(ss, ps, vb):
             self.failed_once.add((s, p))
-            log.commits.append((s, p, v, v, "failed"))
+            self._items.append((s, p, v, v, "failed"))
         log.fallbacks += 1
         for s, p, v, o in zip(ss, ps, vb, g.owners):                    # App. H fallback: singletons
             single = Group(WRITE, [o], g.c.shape_id, g.c.placement, g.c.backend, self.clock)
             capi.write_commit(pool, single, tr.eta, None, stream)
-            log.commits.append((s, p, v, v + 1, "ok"))
+            self._items.append(("single", capi.tttstate_last_commit_seq(pool), o, s, p, v))
+
+    # ---------------------------------------------------------------- confirmation + log
+    def drain(self):
+        """Synchronise, read the device refusal records and expand the provisional commits
+        into the final log: a group with a refused member is logged failed, then each
+        member's singleton outcome (App. H); a refused singleton is logged failed."""
+        pool, log = self.eng.pool, self.log
+        capi.tttstate_sync(pool, self.stream)
+        refused = {(q, o) for o, _v, q in capi.tttstate_refusals(pool, self.stream)}
+        for it in self._items:
+            if it[0] == "group":
+                _, q, mem = it
+                bad = [(q, o) in refused for o, _, _, _ in mem]
+                if any(bad):
+                    log.fallbacks += 1
+                    log.device_failures += 1
+                    for _o, s, p, v in mem:
+                        log.commits.append((s, p, v, v, "failed"))
+                for (_o, s, p, v), b in zip(mem, bad):
+                    log.commits.append((s, p, v, v, "failed") if b else (s, p, v, v + 1, "ok"))
+            elif it[0] == "single":
+                _, q, o, s, p, v = it
+                log.commits.append((s, p, v, v, "failed") if (q, o) in refused else (s, p, v, v + 1, "ok"))
+            else:
+                log.commits.append(it)
+        self._items = []
 
     def finish(self) -> RunLog:
+        self.drain()
         for s, o in enumerate(self.owners):
             self.log.versions[s] = capi.tttstate_version(self.eng.pool, o)
         for b in self.branches:
@@ -228,10 +361,10 @@ class Server:
         return self.log
 
 
-def run_trace(eng: Engine, tr, src: InputSource, stream=None, sync_writes: bool = True,
-              max_clock: int | None = None) -> RunLog:
+def run_trace(eng: Engine, tr, src: InputSource, stream=None, max_clock: int | None = None,
+              native: bool = True) -> RunLog:
     """Alg. 1 over a workload.traces.Trace (App. H: fallback + wait budget)."""
-    srv = Server(eng, tr, src, stream, sync_writes)
+    srv = Server(eng, tr, src, stream, native=native)
     srv.admit()
     while not srv.done():
         if max_clock is not None and srv.clock >= max_clock:

@@ -9,7 +9,7 @@ import numpy as np
 import torch
 
 from oracle import numerics as nm
-from paper_2605_28053_b200.serving import Engine, InputSource
+from paper_2605_28053_b200.serving import Engine, InputSource, StepIO
 
 
 def to_dev(arr: np.ndarray, dtype: str, device) -> torch.Tensor:
@@ -60,6 +60,22 @@ class HostGenInputs(InputSource):
         Yh = to_host_f64(Y)
         for k, (s, p) in enumerate(zip(ss, ps)):
             self.out[(s, p, l)] = Yh[k]
+
+    def step_io(self, ss, ps):
+        tr, L, n = self.tr, len(self.layers), len(ss)
+        X = to_dev(np.stack([np.stack([tr.x(s, p, l) for s, p in zip(ss, ps)]) for l in self.layers]), tr.dtype, self.dev)
+        Vt = to_dev(np.stack([np.stack([tr.tgt(s, p, l) for s, p in zip(ss, ps)]) for l in self.layers]), tr.dtype,
+                    self.dev)
+        Y = torch.empty(L, n, tr.d_model, dtype=X.dtype, device=self.dev)
+        return StepIO(X, n * tr.d_ff, Vt, n * tr.d_model, Y, n * tr.d_model, list(range(n)))
+
+    def on_step(self, executed, io):
+        if not executed:
+            return
+        Yh = to_host_f64(io.Y)
+        for s, p, row in executed:
+            for i, l in enumerate(self.layers):
+                self.out[(s, p, l)] = Yh[i, row]
 
 
 def make_engine(tr, device="cuda", n_ckpt=4, max_owners=None, mode=None, B=None, w=None):
@@ -131,3 +147,20 @@ class DeviceGenInputs(InputSource):
         for k, (s, p) in enumerate(zip(ss, ps)):
             if s in self.record:
                 self.out[(s, p, l)] = to_host_f64(Y[k])
+
+    def step_io(self, ss, ps):
+        tr, rng, L, n = self.tr, self.rng, self.tr.n_layers, len(ss)
+        X = torch.empty(L, n, tr.d_ff, dtype=self.tdt, device=self.dev)
+        Vt = torch.empty(L, n, tr.d_model, dtype=self.tdt, device=self.dev)
+        for l in range(L):
+            for i, (s, p) in enumerate(zip(ss, ps)):
+                self.capi.gen_uniform(X[l, i], tr.seed, rng.T_X, tr.owner(s), l, p, tr.d_ff, 1.0, self.bf16)
+                self.capi.gen_uniform(Vt[l, i], tr.seed, rng.T_TGT, tr.owner(s), l, p, tr.d_model, 1.0, self.bf16)
+        Y = torch.empty(L, n, tr.d_model, dtype=self.tdt, device=self.dev)
+        return StepIO(X, n * tr.d_ff, Vt, n * tr.d_model, Y, n * tr.d_model, list(range(n)))
+
+    def on_step(self, executed, io):
+        for s, p, row in executed:
+            if s in self.record:
+                for l in range(self.tr.n_layers):
+                    self.out[(s, p, l)] = to_host_f64(io.Y[l, row])

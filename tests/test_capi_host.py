@@ -132,3 +132,46 @@ def test_cpp_planner_matches_oracle_planner(mode):
                 waiting -= set(g.owners)
             waiting |= {e.owner for e in oev} - {e.owner for e in orej}
         capi.ttt_planner_destroy(pl)
+
+
+def test_binding_checks_tensor_operands_before_the_call():
+    """tensors handed to read_apply / read_apply_chunk / tail_load / serve_step are
+    checked against the pool's σ.dtype, contiguity, row width and row count; raw integer
+    addresses stay the caller's unchecked opt-in path."""
+    import torch
+    p = _host_pool()                                   # bf16, d_model 8, d_ff 16
+    capi.tttstate_alloc(p, 1)
+    g = capi.Group(capi.READ, [1])
+    X, V, Y = (torch.zeros(1, 16, dtype=torch.bfloat16), torch.zeros(1, 8, dtype=torch.bfloat16),
+               torch.zeros(1, 8, dtype=torch.bfloat16))
+    bad = [(X.float(), V, Y), (torch.zeros(1, 32, dtype=torch.bfloat16)[:, ::2], V, Y),
+           (torch.zeros(1, 8, dtype=torch.bfloat16), V, Y), (X, V, torch.zeros(0, 8, dtype=torch.bfloat16))]
+    for x, v, y in bad:
+        with pytest.raises(ValueError):
+            capi.read_apply(p, g, 0, x, None, v, None, y)
+    with pytest.raises(ValueError):                    # a row map shorter than the group
+        capi.read_apply(p, capi.Group(capi.READ, [1]), 0, X, [], V, None, Y)
+    with pytest.raises(capi.TTTError) as e:            # well-formed operands reach the library
+        capi.read_apply(p, g, 0, X, None, V, None, Y)
+    assert e.value.status == -3                        # TTT_E_NO_DEVICE on a host-only pool
+    capi.tttstate_pool_destroy(p)
+
+
+def test_serve_step_validates_before_side_effects_on_a_host_pool():
+    p = _host_pool()
+    pl = capi.ttt_planner_create(capi.MODE_FULL, 8, 0)
+    capi.ttt_planner_attach(pl, p)
+    for o in (1, 2):
+        capi.tttstate_alloc(p, o)
+    bufs = capi.StepBuffers(16)
+    bufs.owners[0], bufs.owners[1] = 1, 2
+    with pytest.raises(capi.TTTError) as e:
+        capi.tttstate_serve_step(p, pl, bufs, 2, 0, 1 << 20, 16, 2 << 20, 8, 3 << 20, 8, 0.01)
+    assert e.value.status == -3                        # no device: nothing planned, nothing pending
+    assert capi.ttt_planner_pending(pl) == 0
+    bufs.owners[1] = 1
+    with pytest.raises(capi.TTTError):
+        capi.tttstate_serve_step(p, pl, bufs, 2, 0, 1 << 20, 16, 2 << 20, 8, 3 << 20, 8, 0.01)
+    assert capi.tttstate_last_commit_seq(p) == 0
+    capi.ttt_planner_destroy(pl)
+    capi.tttstate_pool_destroy(p)

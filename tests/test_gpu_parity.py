@@ -166,11 +166,37 @@ def test_device_detected_nonfinite_write_fails_group():
     Vt = torch.ones(2, tr.d_model, device=DEV)
     Y = torch.empty(2, tr.d_model, device=DEV)
     capi.read_apply(pool, g, 0, X, None, Vt, None, Y)
-    capi.write_commit(pool, g, tr.eta)                 # optimistic host mirror
-    assert capi.tttstate_sync(pool) == 1               # reconciled
-    assert [capi.tttstate_version(pool, o) for o in owners] == [0, 0]
-    assert [capi.tttstate_device_version(pool, o) for o in owners] == [0, 0]
-    assert capi.tttstate_tail_len(pool, owners[0]) == 0 and capi.tttstate_next_event(pool, owners[0], 0).effect == 1
+    assert capi.write_commit(pool, g, tr.eta) == [1, 1]      # optimistic host mirror, no host sync
+    seq = capi.tttstate_last_commit_seq(pool)
+    # the device fails the group and resolves App. H's singleton retries at once (control.cu):
+    # owner 0's candidate is finite -> published; owner 1's is not -> refused for good (reading xx)
+    assert capi.tttstate_sync(pool) == 1
+    assert capi.tttstate_refusals(pool) == [(owners[1], 0, seq)]
+    assert [capi.tttstate_version(pool, o) for o in owners] == [1, 0]
+    assert [capi.tttstate_device_version(pool, o) for o in owners] == [1, 0]
+    assert [capi.tttstate_tail_len(pool, o) for o in owners] == [0, 0]        # owner 1's evidence dropped
+    assert capi.tttstate_next_event(pool, owners[1], 0).effect == 1 and capi.tttstate_sync(pool) == 0
+
+
+@pytest.mark.parametrize("native", [True, False])
+@pytest.mark.parametrize("dtype,chunk", [("bf16", 4), ("fp32", 4), ("bf16", 1)])
+def test_poisoned_evidence_device_failure_through_the_serving_loop(native, dtype, chunk):
+    """a non-finite candidate (an inf target in the chunk's evidence) fails its WRITE group on
+    the device; App. H's singleton retries publish the clean members and refuse the poisoned one for good
+    (v and bytes kept, evidence dropped).  Logs, versions, outputs and fast weights match the oracle, which
+    follows the same reading (oracle/run.py _retry); snapshots / rollbacks / injected failures around it."""
+    tr = T.uniform_small(n_streams=6, n_layers=2, d_model=128, d_ff=256, chunk=chunk, n_steps=4 * chunk + 2,
+                         dtype=dtype, delta0="rng", v0=2, seed=21,
+                         controls={(1, chunk - 1): ["poison"], (3, 2 * chunk - 1): ["poison", "fail"],
+                                   (4, chunk): ["snapshot"], (4, 2 * chunk + 1): ["rollback"],
+                                   (0, 3 * chunk - 1): ["fail"], (2, 2 * chunk): ["poison"]})
+    ref = run_batched(tr)
+    eng = make_engine(tr, DEV)
+    src = HostGenInputs(tr, DEV)
+    log = run_trace(eng, tr, src, native=native)
+    torch.cuda.synchronize()
+    _compare(tr, ref, src, log, eng)
+    assert log.device_failures >= 2 and any(c[4] == "failed" and c[0] == 1 for c in log.commits)
 
 
 def test_generator_device_matches_numpy():

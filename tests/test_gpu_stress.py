@@ -147,7 +147,7 @@ def _run_scenario(scn):
     inject_at = {"VersionMismatch": 3, "StaleReadAttempt": 5, "OwnerMapCollision": 2}.get(scn)
     serving.capi.write_commit = checked_write_commit
     try:
-        srv = serving.Server(eng, tr, src, None, True)
+        srv = serving.Server(eng, tr, src, None, native=False)   # per-operator calls: state checked between them
         srv.admit()
         path = None
         while not srv.done():

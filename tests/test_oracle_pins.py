@@ -498,3 +498,38 @@ def test_prefill_tail_bursty_trace_first_write_and_closed_form():
         # fp32 storage rounds once per commit: agreement to fp32 precision, while a
         # dropped or duplicated evidence entry moves the state by ~η·|v||z| ≫ 1e-6.
         assert nm.normwise_rel_err(rec.state[s][0], closed) < 1e-6
+
+
+# ---------------------------------------------------------------- device-detected failure (reading xx)
+def test_nonfinite_candidate_fails_group_then_singletons_resolve():
+    """A non-finite candidate fails its WRITE group (nothing commits: S:368); App. H's
+    singleton retries publish the clean members, while the poisoned member fails
+    again (the update is deterministic) and its failure is final: v and ΔW stay, the chunk's
+    evidence is dropped (reading xx), and it goes on decoding from v."""
+    C = 2
+    tr = T.uniform_small(n_streams=3, n_layers=1, d_model=3, d_ff=4, chunk=C, n_steps=6, dtype="fp32",
+                         controls={(1, 1): ["poison"]})
+    rec = run_batched(tr)
+    # step p = 1 is every stream's first WRITE; stream 1's target at p = 1 carries +inf
+    assert rec.commits[:6] == [(0, 1, 0, 0, "failed"), (1, 1, 0, 0, "failed"), (2, 1, 0, 0, "failed"),
+                               (0, 1, 0, 1, "ok"), (1, 1, 0, 0, "failed"), (2, 1, 0, 1, "ok")]
+    assert rec.versions == {0: 3, 1: 2, 2: 3}
+    assert all(np.all(np.isfinite(rec.state[s][0])) for s in range(3))
+    # stream 1 = a clean stream whose first chunk never happened: its later commits use only
+    # evidence of p = 2..5 (closed form from ΔW_0 = 0)
+    Z = np.stack([nm.widen(tr.x(1, p, 0), "fp32") for p in range(2, 6)])
+    Vt = np.stack([nm.widen(tr.tgt(1, p, 0), "fp32") for p in range(2, 6)])
+    assert nm.normwise_rel_err(rec.state[1][0], tr.eta * (Vt.T @ Z)) < 1e-6
+    seq = run_sequential(tr)
+    assert ok_commits(seq) == ok_commits(rec) and seq.versions == rec.versions
+    for s in range(3):
+        assert np.array_equal(seq.state[s][0], rec.state[s][0])
+
+
+def test_drop_chunk_keeps_version_and_payload():
+    tab = _tiny_table(C=2)
+    tab.alloc(5)
+    tab.apply(5, 0, [np.ones(3)], [np.ones(2)])
+    S0 = tab.owners[5].S[0].copy()
+    tab.drop_chunk(5)
+    assert tab.tail_len(5) == 0 and tab.version(5) == 0 and np.array_equal(tab.owners[5].S[0], S0)

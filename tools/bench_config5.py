@@ -59,7 +59,7 @@ def main():
     eng = Engine(tr.d_model, tr.d_ff, tr.chunk, L, "bf16", sh.n_streams, W, n_ckpt=0, B=sh.B, w=0, placement=rank)
     src = WindowInputs(sh, dev)
     stream = torch.cuda.current_stream(dev)
-    srv = Server(eng, sh, src, stream=stream, sync_writes=True)
+    srv = Server(eng, sh, src, stream=stream)
     srv.admit()
     torch.cuda.synchronize(dev)
     del src.d0

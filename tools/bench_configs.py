@@ -31,7 +31,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from paper_2605_28053_b200 import capi  # noqa: E402
-from paper_2605_28053_b200.serving import Engine, InputSource, Server  # noqa: E402
+from paper_2605_28053_b200.serving import Engine, InputSource, Server, StepIO  # noqa: E402
 from workload import rng  # noqa: E402
 from workload import traces as T  # noqa: E402
 
@@ -83,6 +83,11 @@ class WindowInputs(InputSource):
         rows = self._rows
         return self.X[l], rows, self.V[l], rows, self.Y[l], rows
 
+    def step_io(self, ss, ps):
+        S, C, tr = self.tr.n_streams, self.tr.chunk, self.tr
+        rows = [(p % C) * S + s for s, p in zip(ss, ps)]
+        return StepIO(self.X, C * S * tr.d_ff, self.V, C * S * tr.d_model, self.Y, C * S * tr.d_model, rows)
+
 
 def trace_of(name: str):
     if name.startswith("3"):                       # "3" (w = 0) or "3w4", "3w16": bounded wait w
@@ -107,7 +112,7 @@ def run(name: str, windows: int, warmup: int):
                  B=tr.B, w=tr.w, backend=tr.backend, rank=tr.rank)
     src = WindowInputs(tr, dev)
     stream = torch.cuda.current_stream(dev)
-    srv = Server(eng, tr, src, stream=stream, sync_writes=True)
+    srv = Server(eng, tr, src, stream=stream)
     srv.admit()
     torch.cuda.synchronize(dev)
     for _ in range(warmup * tr.chunk):

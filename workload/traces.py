@@ -84,8 +84,14 @@ class Trace:
         return rng.gen(self.seed, rng.T_X, self.owner(s), l, p, (self.d_ff,), 1.0, self.dtype)
 
     def tgt(self, s: int, p: int, l: int) -> np.ndarray:
-        """Update target v for stream s at position p, layer l (reading iii)."""
-        return rng.gen(self.seed, rng.T_TGT, self.owner(s), l, p, (self.d_model,), 1.0, self.dtype)
+        """Update target v for stream s at position p, layer l (reading iii).  A "poison"
+        control at (s, p) makes element 0 +inf (an input fault: the chunk's candidate is then
+        not finite, so its WRITE fails on the device — DESIGN.md reading xx)."""
+        v = rng.gen(self.seed, rng.T_TGT, self.owner(s), l, p, (self.d_model,), 1.0, self.dtype)
+        if "poison" in self.controls_at(s, p):
+            v = v.copy()
+            v[0] = 0x7F80 if self.dtype == "bf16" else np.float32(np.inf)
+        return v
 
     def controls_at(self, s: int, p: int):
         return self.controls.get((s, p), ())
