@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--prefill", type=int, default=0, help="profiling only: initial tail fill (boundary sooner)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config5", action="store_true", help="skip the BJ configs[4] strong-scaling block")
     return ap.parse_args()
 
 
@@ -198,6 +199,137 @@ def run_reference(a, rank, world):
 
 
 # ------------------------------------------------------------------ GPU arm
+def _window_class():
+    import torch
+
+    from paper_2605_28053_b200 import capi
+    from paper_2605_28053_b200.serving import InputSource, StepIO
+    from workload import rng
+
+    class HBMWindow(InputSource):
+        """One chunk window of seeded inputs resident in HBM: X [L][C*S][d_ff], V/Y [L][C*S][d_model]
+        (row (p mod C)*S + s holds stream s's token at position p); initial ΔW_0 per owner."""
+
+        def __init__(self, tr, dev, n_streams, key_owner, prefill=0):
+            L, C, S = tr.n_layers, tr.chunk, n_streams
+            self.tr, self.dev, self.S, self.prefill = tr, dev, S, prefill
+            self.X = torch.empty(L, C * S, tr.d_ff, dtype=torch.bfloat16, device=dev)
+            self.V = torch.empty(L, C * S, tr.d_model, dtype=torch.bfloat16, device=dev)
+            self.Y = torch.empty(L, C * S, tr.d_model, dtype=torch.bfloat16, device=dev)
+            for l in range(L):
+                capi.gen_uniform(self.X[l], SEED, rng.T_X, key_owner, l, 0, self.X[l].numel(), 1.0, True)
+                capi.gen_uniform(self.V[l], SEED, rng.T_TGT, key_owner, l, 0, self.V[l].numel(), 1.0, True)
+            self.d0 = torch.empty(L, tr.d_model, tr.d_ff, dtype=torch.bfloat16, device=dev)
+
+        def init_delta(self, s):
+            tr = self.tr
+            for l in range(tr.n_layers):
+                capi.gen_uniform(self.d0[l], SEED, rng.T_DELTA0, tr.owner(s), l, 0, tr.d_model * tr.d_ff,
+                                 rng.amp_inv_sqrt(tr.d_ff), True)
+            return self.d0
+
+        def tail_prefill(self, s):
+            n, tr = self.prefill, self.tr
+            if not n:
+                return None
+            Z = torch.empty(tr.n_layers, n, tr.d_ff, dtype=torch.bfloat16, device=self.dev)
+            V = torch.empty(tr.n_layers, n, tr.d_model, dtype=torch.bfloat16, device=self.dev)
+            capi.gen_uniform(Z, SEED, rng.T_X, tr.owner(s), 0, -n, Z.numel(), 1.0, True)
+            capi.gen_uniform(V, SEED, rng.T_TGT, tr.owner(s), 0, -n, V.numel(), 1.0, True)
+            return n, Z, V
+
+        def step_io(self, ss, ps):               # the native step: one row map for every layer
+            C, S, tr = self.tr.chunk, self.S, self.tr
+            rows = [(p % C) * S + s for s, p in zip(ss, ps)]
+            return StepIO(self.X, C * S * tr.d_ff, self.V, C * S * tr.d_model, self.Y, C * S * tr.d_model, rows)
+
+    return HBMWindow
+
+
+C5_ROOFLINE = {1: 32800.0, 2: 65300.0, 4: 129600.0, 8: 255400.0}   # SURVEY §8(d) config 5, tok/s aggregate
+
+
+def config5_block(dev, rank, world, coll_dev, shard_world=None, shard_rank=None):
+    """BJ configs[4]: 256 streams sharded by owner, π(o) = s mod G, 64K
+    context (v0 = 512), L = 4, paper dims, bf16 — STRONG scaling (total work fixed as G grows).
+    Each rank serves its shard through the native serving step (one tttstate_serve_step call per
+    decode step) with its own pool, planner and W_down replica; NCCL carries the barrier, the MAX
+    of window times and the digest gather only.  One 128-step window after a warm-up window.
+    With shard_world set, one process times the shard a rank of a G-GPU run would serve
+    (the host-overhead check at the G = 8 per-rank shape on one GPU)."""
+    import hashlib
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_28053_b200 import capi
+    from paper_2605_28053_b200 import distributed as D
+    from paper_2605_28053_b200.serving import Engine, Server
+    from workload import rng
+    from workload import traces as T
+
+    G = shard_world or world
+    r = rank if shard_rank is None else shard_rank
+    tr = T.config5_sharded(n_steps=1 << 30)
+    sh = T.shard(tr, G, r)
+    L = tr.n_layers
+    W = torch.empty(L, tr.d_model, tr.d_ff, dtype=torch.bfloat16, device=dev)
+    for l in range(L):
+        capi.gen_uniform(W[l], SEED, rng.T_W_DOWN, 0, l, 0, tr.d_model * tr.d_ff, rng.amp_inv_sqrt(tr.d_ff), True)
+    eng = Engine(tr.d_model, tr.d_ff, tr.chunk, L, "bf16", sh.n_streams, W, n_ckpt=0, B=sh.B, w=0, placement=r)
+    src = _window_class()(sh, dev, sh.n_streams, sh.owner(0))
+    stream = torch.cuda.current_stream(dev)
+    srv = Server(eng, sh, src, stream=stream)
+    srv.admit()
+    torch.cuda.synchronize(dev)
+    del src.d0
+    for _ in range(tr.chunk):                                   # warm-up window
+        srv.step()
+    torch.cuda.synchronize(dev)
+    if world > 1 and shard_world is None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    c0 = sum(srv.log.census.values())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(tr.chunk):
+        srv.step()
+    e1.record(stream)
+    t_enq = time.perf_counter() - t0
+    torch.cuda.synchronize(dev)
+    t_wall = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1)
+    tokens = sum(srv.log.census.values()) - c0
+    dig = hashlib.sha256(src.Y.contiguous().view(torch.uint8).cpu().numpy().tobytes()).hexdigest()
+    log = srv.finish()
+    out = {"device_ms_per_step": ms / tr.chunk, "host_enqueue_ms_per_step": 1e3 * t_enq / tr.chunk,
+           "host_wall_ms_per_step": 1e3 * t_wall / tr.chunk, "host_wall_over_device": 1e3 * t_wall / ms,
+           "tokens": tokens, "versions": sorted(set(log.versions.values())), "digest": dig}
+    eng.close()
+    del srv, src, W, eng
+    torch.cuda.empty_cache()
+    if shard_world is not None:
+        out.update({"shape": f"one rank's shard of a G = {G} run: {sh.n_streams} streams x {L} layers",
+                    "tok_s": tokens / (ms / 1e3)})
+        return out
+    ms_max = D.max_over_ranks(ms, coll_dev)
+    tok_total = D.sum_over_ranks(tokens, coll_dev)
+    digests = {str(k): v for k, v in sorted(D.gather_dict({rank: dig}).items())}
+    tok_s = tok_total / (ms_max / 1e3)
+    roof = C5_ROOFLINE.get(world)
+    out.update({"workload": "config5_sharded: 256 TTT streams sharded by owner (pi(o) = s mod G), L=4, d_model=2560, "
+                            "d_ff=9728, bf16, C=128, 64K ctx (v0=512, random dW), uniform, B = 256/G, w=0",
+                "scaling": "strong", "G": world, "streams_total": tr.n_streams, "streams_per_rank": sh.n_streams,
+                "window_steps": tr.chunk, "ms_per_step_max_over_ranks": ms_max / tr.chunk, "value": tok_s,
+                "unit": "tok/s", "roofline_tok_s": roof, "frac_of_roofline": tok_s / roof if roof else None,
+                "digests_by_rank": digests,
+                "roofline_basis": "SURVEY §8(d): per GPU per step 4 x (E x 2 + (256/G) x E x 2) bytes at MP hbm_gbs"})
+    out.pop("digest")
+    return out
+
+
 def main():
     a = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -242,45 +374,6 @@ def main():
         capi.gen_uniform(W[l], SEED, rng.T_W_DOWN, 0, l, 0, D_MODEL * D_FF, amp, True)
     eng = Engine(D_MODEL, D_FF, CHUNK, L, "bf16", N_STREAMS, W, n_ckpt=0, B=8, w=0, placement=rank)
 
-    class Window(InputSource):
-        """One chunk window of inputs resident in HBM: X [L][C*8][d_ff], V [L][C*8][d_model]."""
-
-        def __init__(self):
-            self.X = torch.empty(L, CHUNK * N_STREAMS, D_FF, dtype=torch.bfloat16, device=dev)
-            self.V = torch.empty(L, CHUNK * N_STREAMS, D_MODEL, dtype=torch.bfloat16, device=dev)
-            self.Y = torch.empty(L, CHUNK * N_STREAMS, D_MODEL, dtype=torch.bfloat16, device=dev)
-            for l in range(L):
-                capi.gen_uniform(self.X[l], SEED, rng.T_X, owner_base, l, 0, self.X[l].numel(), 1.0, True)
-                capi.gen_uniform(self.V[l], SEED, rng.T_TGT, owner_base, l, 0, self.V[l].numel(), 1.0, True)
-            self.d0 = torch.empty(L, D_MODEL, D_FF, dtype=torch.bfloat16, device=dev)
-
-        def init_delta(self, s):
-            for l in range(L):
-                capi.gen_uniform(self.d0[l], SEED, rng.T_DELTA0, tr.owner(s), l, 0, D_MODEL * D_FF, amp, True)
-            return self.d0
-
-        def tail_prefill(self, s):
-            n = a.prefill
-            if not n:
-                return None
-            Z = torch.empty(L, n, D_FF, dtype=torch.bfloat16, device=dev)
-            V = torch.empty(L, n, D_MODEL, dtype=torch.bfloat16, device=dev)
-            capi.gen_uniform(Z, SEED, rng.T_X, tr.owner(s), 0, -n, Z.numel(), 1.0, True)
-            capi.gen_uniform(V, SEED, rng.T_TGT, tr.owner(s), 0, -n, V.numel(), 1.0, True)
-            return n, Z, V
-
-        def group_io(self, l, ss, ps):
-            key = (tuple(ss), tuple(ps))
-            if key != getattr(self, "_key", None):     # one row map per step, reused by every layer
-                self._key, self._rows = key, capi.rows_array([(p % CHUNK) * N_STREAMS + s for s, p in zip(ss, ps)])
-            rows = self._rows
-            return self.X[l], rows, self.V[l], rows, self.Y[l], rows
-
-        def step_io(self, ss, ps):               # the native step: one row map for every layer
-            rows = [(p % CHUNK) * N_STREAMS + s for s, p in zip(ss, ps)]
-            return StepIO(self.X, CHUNK * N_STREAMS * D_FF, self.V, CHUNK * N_STREAMS * D_MODEL, self.Y,
-                          CHUNK * N_STREAMS * D_MODEL, rows)
-
     # start of run (SURVEY §8(e) 1): rank 0's config and owner→rank map to every rank; each
     # rank checks that the owners it serves are exactly the ones the map places on it
     run_cfg = D.broadcast_config({"n_streams_per_rank": N_STREAMS, "layers": L, "chunk": CHUNK,
@@ -288,7 +381,7 @@ def main():
                                                 for s in range(N_STREAMS)}} if rank == 0 else None)
     assert sorted(o for o, r in run_cfg["placement"].items() if r == rank) == \
         [tr.owner(s) for s in range(N_STREAMS)], "owner map disagrees with this rank's owners"
-    src = Window()
+    src = _window_class()(tr, dev, N_STREAMS, owner_base, a.prefill)
     stream = torch.cuda.current_stream(dev)
     srv = Server(eng, tr, src, stream=stream, profile=True, profile_every=8)
     srv.admit()
@@ -424,6 +517,19 @@ def main():
                "h2d_bytes_per_step": (Xh.numel() + Vh.numel()) * 2, "d2h_bytes_per_step": Yh.numel() * 2,
                "overlap": "double-buffered windows: H2D(k+1) and D2H(k-1) on a copy stream during compute(k)"}
 
+    # ---- BJ configs[4] strong-scaling block (the north_star scaling target: 256 streams over
+    # N GPUs) and, at N = 1, the G = 8 per-rank shape for the host-overhead check
+    c5 = c5_g8 = None
+    if not a.no_config5:
+        eng.close()
+        del srv, src, W, eng
+        if not a.no_e2e:
+            del bufs, Xh, Vh, Yh
+        torch.cuda.empty_cache()
+        c5 = config5_block(dev, rank, world, coll_dev)
+        if world == 1:
+            c5_g8 = config5_block(dev, rank, world, coll_dev, shard_world=8, shard_rank=0)
+
     if rank == 0:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         hbm = peaks["hbm_gbs"]
@@ -497,6 +603,8 @@ def main():
             "planner_host_share": plan_s / wall_s,
             "host_wall_ms_per_step": wall_s * 1e3 / a.steps,
             "clocks": clk.summary(),
+            "config5_strong": c5,
+            "config5_g8_rank_shape_on_1_gpu": c5_g8,
             "output_digest": {"sha256_by_rank": digests,
                               "what": "bf16 Y of every layer for the last timed window (all streams x C "
                                       "positions); fixed-order reductions: identical on reruns"},

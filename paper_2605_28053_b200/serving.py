@@ -149,6 +149,7 @@ class Server:
         self.plan_s = 0.0                 # host seconds in View/controls + marshalling (P:525's overhead share)
         self._items: list = []            # commit log items, expanded by drain() (provisional commits)
         self._has_controls = bool(tr.controls)
+        self._vtrue = {s: tr.v0 for s in range(tr.n_streams)}   # confirmed version replay (drain)
         self.bufs = capi.StepBuffers(eng.max_owners)
         self._wev = self._fresh_pair() if profile else (None, None)
 
@@ -187,7 +188,7 @@ class Server:
             elif op == "rollback":
                 vb = capi.tttstate_version(pool, o)
                 va = capi.rollback(pool, o, stream)
-                self._items.append((s, self.pos[s], vb, va, "rolled_back"))
+                self._items.append(("rb", s, self.pos[s], vb, va))
             elif op == "fork":                                  # new lineage
                 k = self.forks.get(s, 0)
                 capi.tttstate_fork(pool, o, tr.branch_owner(s, k), stream)
@@ -247,14 +248,14 @@ class Server:
                 n_read_launches += (len(ss) + 7) // 8
             else:
                 if inj:
-                    for s, p, v in zip(ss, ps, vb):
+                    for s, p in zip(ss, ps):
                         self.failed_once.add((s, p))
-                        self._items.append((s, p, v, v, "failed"))
+                        self._items.append(("fail", s, p))
                     log.fallbacks += 1
-                    for o, s, p, v, q in zip(owners, ss, ps, vb, seqs):   # singleton retries
-                        self._items.append(("single", q, o, s, p, v))
+                    for o, s, p, q in zip(owners, ss, ps, seqs):   # singleton retries
+                        self._items.append(("single", q, o, s, p))
                 else:
-                    self._items.append(("group", seqs[0], list(zip(owners, ss, ps, vb))))
+                    self._items.append(("group", seqs[0], list(zip(owners, ss, ps))))
             for s in ss:
                 executed.append((s, self.pos[s], row_of[s]))
                 self.pos[s] += 1
@@ -308,48 +309,60 @@ class Server:
 
     def _write_percall(self, g, ss, ps):
         tr, log, stream, pool = self.tr, self.log, self.stream, self.eng.pool
-        vb = [capi.tttstate_version(pool, o) for o in g.owners]
         mask = [self._injected(s) for s in ss]
         try:                                                            # CommitVersions
             capi.write_commit(pool, g, tr.eta, mask if any(mask) else None, stream)
-            self._items.append(("group", capi.tttstate_last_commit_seq(pool), list(zip(g.owners, ss, ps, vb))))
+            self._items.append(("group", capi.tttstate_last_commit_seq(pool), list(zip(g.owners, ss, ps))))
             return
         except TTTError as e:
             if e.status != capi.TTT_E_WRITE_FAILED:
                 raise
-        for s, p, v in zip(ss, ps, vb):
+        for s, p in zip(ss, ps):
             self.failed_once.add((s, p))
-            self._items.append((s, p, v, v, "failed"))
+            self._items.append(("fail", s, p))
         log.fallbacks += 1
-        for s, p, v, o in zip(ss, ps, vb, g.owners):                    # App. H fallback: singletons
+        for s, p, o in zip(ss, ps, g.owners):                           # App. H fallback: singletons
             single = Group(WRITE, [o], g.c.shape_id, g.c.placement, g.c.backend, self.clock)
             capi.write_commit(pool, single, tr.eta, None, stream)
-            self._items.append(("single", capi.tttstate_last_commit_seq(pool), o, s, p, v))
+            self._items.append(("single", capi.tttstate_last_commit_seq(pool), o, s, p))
 
     # ---------------------------------------------------------------- confirmation + log
     def drain(self):
         """Synchronise, read the device refusal records and expand the provisional commits
-        into the final log: a group with a refused member is logged failed, then each
-        member's singleton outcome (App. H); a refused singleton is logged failed."""
+        into the final log, replaying each stream's committed version (the host mirror's
+        versions are provisional while commits are unconfirmed): a group with a refused member
+        is logged failed, then each member's singleton outcome (App. H); a refused singleton
+        is logged failed."""
         pool, log = self.eng.pool, self.log
         capi.tttstate_sync(pool, self.stream)
         refused = {(q, o) for o, _v, q in capi.tttstate_refusals(pool, self.stream)}
+        vt = self._vtrue
+
+        def one(s, p, ok):
+            v = vt[s]
+            log.commits.append((s, p, v, v + 1, "ok") if ok else (s, p, v, v, "failed"))
+            vt[s] = v + 1 if ok else v
+
         for it in self._items:
             if it[0] == "group":
                 _, q, mem = it
-                bad = [(q, o) in refused for o, _, _, _ in mem]
+                bad = [(q, o) in refused for o, _, _ in mem]
                 if any(bad):
                     log.fallbacks += 1
                     log.device_failures += 1
-                    for _o, s, p, v in mem:
-                        log.commits.append((s, p, v, v, "failed"))
-                for (_o, s, p, v), b in zip(mem, bad):
-                    log.commits.append((s, p, v, v, "failed") if b else (s, p, v, v + 1, "ok"))
+                    for _o, s, p in mem:
+                        one(s, p, False)
+                for (_o, s, p), b in zip(mem, bad):
+                    one(s, p, not b)
             elif it[0] == "single":
-                _, q, o, s, p, v = it
-                log.commits.append((s, p, v, v, "failed") if (q, o) in refused else (s, p, v, v + 1, "ok"))
-            else:
-                log.commits.append(it)
+                _, q, o, s, p = it
+                one(s, p, (q, o) not in refused)
+            elif it[0] == "fail":
+                one(it[1], it[2], False)
+            else:                                               # ("rb", s, p, v_before, v_after)
+                _, s, p, vb, va = it
+                log.commits.append((s, p, vb, va, "rolled_back"))
+                vt[s] = va
         self._items = []
 
     def finish(self) -> RunLog:

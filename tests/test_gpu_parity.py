@@ -196,7 +196,9 @@ def test_poisoned_evidence_device_failure_through_the_serving_loop(native, dtype
     log = run_trace(eng, tr, src, native=native)
     torch.cuda.synchronize()
     _compare(tr, ref, src, log, eng)
-    assert log.device_failures >= 2 and any(c[4] == "failed" and c[0] == 1 for c in log.commits)
+    assert log.device_failures >= 1
+    finals = {s for s in (1, 2, 3) if sum(c[0] == s and c[4] == "failed" for c in log.commits) >= 2}
+    assert finals == {1, 2, 3}          # group attempt + final singleton failure of every poisoned stream
 
 
 def test_generator_device_matches_numpy():

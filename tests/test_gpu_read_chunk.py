@@ -86,8 +86,12 @@ def test_chunk_read_contract_errors():
         capi.write_commit(eng.pool, g, 0.01)                   # layer 1 not applied yet
     assert e.value.status == 7
     with pytest.raises(capi.TTTError) as e:                    # decode READ mid-chunk is refused
-        capi.read_apply(eng.pool, capi.Group(capi.READ, owners), 1, X[:, 0], None, V[:, 0], None, Y[:, 0])
+        capi.read_apply(eng.pool, capi.Group(capi.READ, owners), 1, X[:, 0].contiguous(), None,
+                        V[:, 0].contiguous(), None, Y[:, 0].contiguous())
     assert e.value.status == 13
     capi.read_apply_chunk(eng.pool, g, 1, X, V, Y)
+    with pytest.raises(capi.TTTError) as e:                    # a chunk ends in write_commit,
+        capi.tttstate_step_done(eng.pool, capi.Group(capi.READ, owners))   # not in a READ step_done
+    assert e.value.status == 13 and capi.tttstate_tail_len(eng.pool, owners[0]) == tr.chunk - 1
     assert capi.write_commit(eng.pool, g, 0.01) == [1, 1]
     assert capi.tttstate_tail_len(eng.pool, owners[0]) == 0
