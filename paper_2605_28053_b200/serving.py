@@ -80,6 +80,7 @@ class RunLog:
     fallbacks: int = 0
     device_failures: int = 0                        # groups with a member refused on the device
     rejected: int = 0                               # planner rejections (re-extracted next step)
+    rollbacks: int = 0
     branches: dict = field(default_factory=dict)    # live branch owner -> version
 
 
@@ -189,6 +190,7 @@ class Server:
                 vb = capi.tttstate_version(pool, o)
                 va = capi.rollback(pool, o, stream)
                 self._items.append(("rb", s, self.pos[s], vb, va))
+                log.rollbacks += 1
             elif op == "fork":                                  # new lineage
                 k = self.forks.get(s, 0)
                 capi.tttstate_fork(pool, o, tr.branch_owner(s, k), stream)

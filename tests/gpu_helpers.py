@@ -122,6 +122,11 @@ class DeviceGenInputs(InputSource):
         tr, rng = self.tr, self.rng
         if tr.delta0 == "zero":
             return None
+        if tr.backend == 1:                      # low-rank payload per layer: A (R·d_ff) then B (R·d_model)
+            return torch.stack([torch.cat([self._gen((tr.rank * tr.d_ff,), rng.T_LR_A, tr.owner(s), l, 0, tr.amp_w),
+                                           self._gen((tr.rank * tr.d_model,), rng.T_LR_B, tr.owner(s), l, 0,
+                                                     rng.amp_inv_sqrt(tr.rank))])
+                                for l in range(tr.n_layers)])
         return torch.stack([self._gen((tr.d_model, tr.d_ff), rng.T_DELTA0, tr.owner(s), l, 0, tr.amp_w)
                             for l in range(tr.n_layers)])
 

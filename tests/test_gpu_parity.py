@@ -35,12 +35,23 @@ def _compare(tr, ref, src, log, eng):
     assert log.commits == ref.commits
     assert log.census == ref.census
     assert log.plan == ref.plan
-    werr = 0.0
+    werr, n_eq, n_all = 0.0, 0, 0
     for s in range(tr.n_streams):
         for l in range(tr.n_layers):
-            got = capi.tttstate_read_payload(eng.pool, tr.owner(s), l, tr.d_model, tr.d_ff, tr.dtype)
-            werr = max(werr, nm.normwise_rel_err(nm.widen(got, tr.dtype), ref.state[s][l]))
+            got = nm.widen(capi.tttstate_read_payload(eng.pool, tr.owner(s), l, tr.d_model, tr.d_ff, tr.dtype), tr.dtype)
+            werr = max(werr, nm.normwise_rel_err(got, ref.state[s][l]))
+            n_eq += int(np.sum(got == ref.state[s][l]))
+            n_all += got.size
     assert werr <= tol, f"fast weights: normwise err {werr} > {tol}"
+    # the oracle mirrors the storage rounding (reading xi), so the committed bytes differ only
+    # where fp32 accumulation order flips a rounding: bf16 (8-bit mantissa) >= 99 % bit-equal
+    if tr.dtype == "bf16":
+        assert n_eq / n_all >= 0.99, f"committed bf16 fast weights bit-equal in {n_eq / n_all:.4f} < 0.99"
+    # elementwise p99 relative error of the READ outputs: reported for information (reading xii)
+    p99 = float(np.percentile(np.concatenate([np.abs(src.out[k] - ref.outputs[k]) / (np.abs(ref.outputs[k]) + 1e-30)
+                                              for k in list(ref.outputs)[:512]]), 99))
+    print(f"parity {tr.name}: READ normwise {worst:.2e} (elementwise p99 {p99:.2e}), fast weights {werr:.2e}, "
+          f"bit-equal {n_eq / n_all:.4f}")
     return worst, werr
 
 

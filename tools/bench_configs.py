@@ -89,9 +89,10 @@ class WindowInputs(InputSource):
         return StepIO(self.X, C * S * tr.d_ff, self.V, C * S * tr.d_model, self.Y, C * S * tr.d_model, rows)
 
 
-def trace_of(name: str):
+def trace_of(name: str, warmup: int = 1):
     if name.startswith("3"):                       # "3" (w = 0) or "3w4", "3w16": bounded wait w
-        return T.config3_interleaved(n_steps=1 << 30, w=int(name[2:]) if "w" in name else 0)
+        # failures / snapshots / rollbacks in the first timed window (after `warmup` windows)
+        return T.config3_interleaved(n_steps=1 << 30, w=int(name[2:]) if "w" in name else 0, control_chunk=warmup)
     if name.startswith("4r"):
         return T.config4_lowrank(n_steps=1 << 16, rank=int(name[2:]))
     if name == "5":
@@ -99,9 +100,46 @@ def trace_of(name: str):
     raise ValueError(name)
 
 
+def sampled_parity(srv, eng, tr, src, W):
+    """The oracle's READ (oracle/numerics.apply_read, oracle/lowrank.apply_read; fp64) on the last
+    decode step of the timed window for streams {0, S-1} x layers {0, L-1}, at the payload version
+    that step read: the committed slot, or the slot the step's own commit retired when that step
+    was the stream's WRITE (reading xvii).  Normwise error against BJ's 2e-2 bound."""
+    import numpy as np
+
+    from oracle import lowrank as olr
+    from oracle import numerics as nm
+
+    capi.tttstate_sync(eng.pool)
+    worst, n = 0.0, 0
+    E = tr.rank * (tr.d_ff + tr.d_model) if tr.backend == 1 else tr.d_model * tr.d_ff
+    for s in (0, tr.n_streams - 1):
+        p = srv.pos[s] - 1
+        was_write = (p + tr.offset(s)) % tr.chunk == tr.chunk - 1
+        dsel = capi.tttstate_read_slot_raw(eng.pool, tr.owner(s), -1, 0, 1, E, "bf16")
+        slots = [capi.tttstate_read_slot_raw(eng.pool, tr.owner(s), w, 0, 1, E, "bf16") for w in (0, 1)]
+        active = 0 if np.array_equal(slots[0], dsel) and not np.array_equal(slots[1], dsel) else 1
+        which = 1 - active if was_write else active
+        row = (p % tr.chunk) * tr.n_streams + s
+        for l in sorted({0, tr.n_layers - 1}):
+            pay = nm.widen(capi.tttstate_read_slot_raw(eng.pool, tr.owner(s), which, l, 1, E, "bf16")[0], "bf16")
+            Wl = nm.widen(W[l].view(torch.int16).cpu().numpy().view(np.uint16), "bf16")
+            x = nm.widen(src.X[l, row].view(torch.int16).cpu().numpy().view(np.uint16), "bf16")
+            y = nm.widen(src.Y[l, row].view(torch.int16).cpu().numpy().view(np.uint16), "bf16")
+            if tr.backend == 1:
+                A = pay[: tr.rank * tr.d_ff].reshape(tr.rank, tr.d_ff)
+                B = pay[tr.rank * tr.d_ff:].reshape(tr.rank, tr.d_model)
+                ref = olr.apply_read(Wl, A, B, x)
+            else:
+                ref = nm.apply_read(Wl, pay.reshape(tr.d_model, tr.d_ff), x)
+            worst = max(worst, nm.normwise_rel_err(y, ref))
+            n += 1
+    return {"samples": n, "max_normwise_err": worst, "tol": nm.TOL["bf16"], "ok": bool(worst <= nm.TOL["bf16"])}
+
+
 def run(name: str, windows: int, warmup: int):
     dev = torch.device("cuda")
-    tr = trace_of(name)
+    tr = trace_of(name, warmup)
     L = tr.n_layers
     W = torch.empty(L, tr.d_model, tr.d_ff, dtype=torch.bfloat16, device=dev)
     for l in range(L):
@@ -118,9 +156,10 @@ def run(name: str, windows: int, warmup: int):
     for _ in range(warmup * tr.chunk):
         srv.step()
     torch.cuda.synchronize(dev)
+    srv.drain()
     census0 = dict(srv.log.census)
     fb0, df0 = srv.log.fallbacks, srv.log.device_failures
-    rb0 = sum(1 for c in srv.log.commits if c[4] == "rolled_back")
+    rb0 = srv.log.rollbacks
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(windows * tr.chunk):
@@ -128,14 +167,17 @@ def run(name: str, windows: int, warmup: int):
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
+    srv.drain()                                    # confirm the window's commits (device refusals)
     tokens = sum(srv.log.census.values()) - sum(census0.values())
     out = {"config": name, "trace": tr.name, "streams": tr.n_streams, "layers": L, "rank": tr.rank or None,
            "B": tr.B, "w": tr.w, "window_steps": windows * tr.chunk, "ms": ms, "tok_s": tokens / (ms / 1e3),
            "census": {"READ": srv.log.census[0] - census0.get(0, 0), "WRITE": srv.log.census[1] - census0.get(1, 0)},
            "fallbacks": srv.log.fallbacks - fb0, "device_failures": srv.log.device_failures - df0,
-           "rollbacks": sum(1 for c in srv.log.commits if c[4] == "rolled_back") - rb0,
+           "rollbacks": srv.log.rollbacks - rb0,
            "roofline_tok_s": ROOFLINE.get(name)}
     out["frac_of_roofline"] = out["tok_s"] / out["roofline_tok_s"] if out["roofline_tok_s"] else None
+    out["parity"] = sampled_parity(srv, eng, tr, src, W)
+    assert out["parity"]["ok"], out["parity"]
     eng.close()
     del src, W, eng
     torch.cuda.empty_cache()

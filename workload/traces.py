@@ -129,15 +129,17 @@ def config2_paper(seed: int = 0, n_steps: int = 512, n_layers: int = 36) -> Trac
 
 
 def config3_interleaved(seed: int = 0, n_steps: int = 512, n_layers: int = 12, w: int = 4,
-                        d_model: int = 2560, d_ff: int = 9728, chunk: int = 128) -> Trace:
+                        d_model: int = 2560, d_ff: int = 9728, chunk: int = 128, control_chunk: int = 0) -> Trace:
     """BJ configs[2]: 64 streams, L=12 (memory), bursty offsets, injected write
-    failures on 1/16 of the streams' first boundary, speculative snapshot + rollback on 1/8."""
+    failures on 1/16 of the streams' boundary in chunk `control_chunk`, speculative snapshot +
+    rollback on 1/8 (control_chunk = 1 puts them inside a timed window after one warm-up window)."""
     offs = bursty_offsets(64, chunk, seed)
     ctl = {}
+    base = control_chunk * chunk
     for s in range(0, 64, 16):                     # injected write failures
-        ctl.setdefault((s, chunk - 1 - offs[s]), []).append("fail")
+        ctl.setdefault((s, base + chunk - 1 - offs[s]), []).append("fail")
     for s in range(3, 64, 8):                      # speculative snapshot + rollback
-        p = chunk - 1 - offs[s]
+        p = base + chunk - 1 - offs[s]
         ctl.setdefault((s, p), []).append("snapshot")
         ctl.setdefault((s, p + 1), []).append("rollback")
     return Trace("config3_interleaved", n_streams=64, n_layers=n_layers, d_model=d_model, d_ff=d_ff,
@@ -154,7 +156,7 @@ def config5_sharded(seed: int = 0, n_steps: int = 512, n_layers: int = 4, d_mode
 
 def config4_lowrank(seed: int = 0, n_steps: int = 512, n_layers: int = 36, rank: int = 16,
                     d_model: int = 2560, d_ff: int = 9728, chunk: int = 128, n_streams: int = 128,
-                    accept_p: float = 0.75) -> Trace:
+                    accept_p: float = 0.75, offset: int = 0) -> Trace:
     """BJ configs[3]: low-rank delta TTTState (R = 16 or 64), 128 streams, speculative branch
     versions: at every boundary each stream forks a branch lineage and snapshots; the
     speculative WRITE is accepted with p = 0.75 (seeded) or rolled back; the previous
@@ -163,7 +165,7 @@ def config4_lowrank(seed: int = 0, n_steps: int = 512, n_layers: int = 36, rank:
     u = rng.raw_u24(seed, 98, 0, 0, 0, n_streams * (n_steps // chunk + 1)) + (1 << 23)
     k = 0
     for s in range(n_streams):
-        for b, p in enumerate(range(chunk - 1, n_steps, chunk)):
+        for b, p in enumerate(range(chunk - 1 - offset, n_steps, chunk)):
             ops = ctl.setdefault((s, p), [])
             if b > 0:
                 ops.append("release")
@@ -173,7 +175,7 @@ def config4_lowrank(seed: int = 0, n_steps: int = 512, n_layers: int = 36, rank:
             k += 1
     return Trace("config4_lowrank", n_streams=n_streams, n_layers=n_layers, d_model=d_model, d_ff=d_ff,
                  chunk=chunk, n_steps=n_steps, dtype="bf16", seed=seed, v0=0, delta0="rng", controls=ctl,
-                 B=n_streams, w=0, backend=1, rank=rank)
+                 B=n_streams, w=0, backend=1, rank=rank, offsets=(offset,) * n_streams if offset else ())
 
 
 def shard(tr: Trace, world: int, rank: int) -> Trace:
