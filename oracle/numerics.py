@@ -52,9 +52,15 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
 
 
 def to_storage(x: np.ndarray, dtype: str) -> np.ndarray:
-    """Value of `x` after being stored in the declared storage dtype."""
+    """Value of the exact candidate `x` after being stored in the declared storage dtype.
+
+    Reading xi: "bf16 storage uses RNE from fp32 accumulators, once per version" — the value
+    rounded to bf16 is the fp32 accumulator, so the mirror first rounds the exact candidate to
+    fp32 (round to nearest even) and then applies the bf16 RNE; storage rounding is a decision
+    taken in the kernel's precision, and both sides take it there.
+    """
     if dtype == "bf16":
-        return round_bf16(x)
+        return round_bf16(np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64))
     if dtype == "fp32":
         return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
     raise ValueError(dtype)

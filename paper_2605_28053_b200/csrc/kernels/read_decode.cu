@@ -116,19 +116,24 @@ template <> struct Elem<float> {
 // shadow slot while the pre-update row is in registers (y uses version v,
 // reading xvii), so an all-update step streams ΔW once in and once out instead
 // of READ + a separate WRITE pass (all-update row P:559).
-__device__ __forceinline__ uint32_t upd_bf16x2(uint32_t w, uint32_t x, float ev, uint32_t &expmax) {
-  const float lo = fmaf(ev, __uint_as_float(x << 16), __uint_as_float(w << 16));
-  const float hi = fmaf(ev, __uint_as_float(x & 0xffff0000u), __uint_as_float(w & 0xffff0000u));
+// The candidate is ΔW + η·(v·x) with v·x exact in fp32 (two 8-bit significands) and ONE fp32
+// rounding of the fma — the fp32 value the storage RNE rounds (reading xi); η·v rounded first
+// would add a second rounding that shifts ~0.5 % of the bf16 results at η = 0.01.
+__device__ __forceinline__ uint32_t upd_bf16x2(uint32_t w, uint32_t x, u64 v2, u64 eta2, uint32_t &expmax) {
+  u64 px, r2 = pack2(w << 16, w & 0xffff0000u);
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(px) : "l"(pack2(x << 16, x & 0xffff0000u)), "l"(v2));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r2) : "l"(px), "l"(eta2));
   uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float((uint32_t)(r2 >> 32))), "f"(__uint_as_float((uint32_t)r2)));
   expmax = __vmaxu2(expmax, r & 0x7f807f80u);
   return r;
 }
 template <typename T> struct Upd;
 template <> struct Upd<__nv_bfloat16> {
-  __device__ static __forceinline__ uint4 apply(const uint4 &w, const uint4 &x, float ev, uint32_t &em) {
-    return make_uint4(upd_bf16x2(w.x, x.x, ev, em), upd_bf16x2(w.y, x.y, ev, em), upd_bf16x2(w.z, x.z, ev, em),
-                      upd_bf16x2(w.w, x.w, ev, em));
+  __device__ static __forceinline__ uint4 apply(const uint4 &w, const uint4 &x, float v, float eta, uint32_t &em) {
+    const u64 v2 = pack2(__float_as_uint(v), __float_as_uint(v)), e2 = pack2(__float_as_uint(eta), __float_as_uint(eta));
+    return make_uint4(upd_bf16x2(w.x, x.x, v2, e2, em), upd_bf16x2(w.y, x.y, v2, e2, em),
+                      upd_bf16x2(w.z, x.z, v2, e2, em), upd_bf16x2(w.w, x.w, v2, e2, em));
   }
   __device__ static __forceinline__ bool bad(uint32_t em) {
     return (em & 0x7f80u) == 0x7f80u || (em >> 16) == 0x7f80u;
@@ -140,7 +145,8 @@ template <> struct Upd<float> {
     em |= isfinite(r) ? 0u : 1u;
     return __float_as_uint(r);
   }
-  __device__ static __forceinline__ uint4 apply(const uint4 &w, const uint4 &x, float ev, uint32_t &em) {
+  __device__ static __forceinline__ uint4 apply(const uint4 &w, const uint4 &x, float v, float eta, uint32_t &em) {
+    const float ev = eta * v;
     return make_uint4(one(w.x, x.x, ev, em), one(w.y, x.y, ev, em), one(w.z, x.z, ev, em), one(w.w, x.w, ev, em));
   }
   __device__ static __forceinline__ bool bad(uint32_t em) { return em != 0; }
@@ -264,12 +270,12 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
         if (v + 32 * u < nvec) E::dot(acc[u % kMaxReadMembers], cur[u], xb[v + 32 * u]);
       if (FUSE) {
         const int b = m - 1, i = t - m * dm;
-        const float ev = p.eta * E::to_f(static_cast<const T *>(p.Vt)[(size_t)p.v_row[b] * dm + i]);
+        const float ev = E::to_f(static_cast<const T *>(p.Vt)[(size_t)p.v_row[b] * dm + i]);
         uint4 *drow = s_dst0[b] + (size_t)i * nvec;
 #pragma unroll
         for (int u = 0; u < kU; ++u)
           // candidate rows are not read again by this step: streaming stores (+2 % measured)
-          if (v + 32 * u < nvec) __stcs(drow + v + 32 * u, Upd<T>::apply(cur[u], xb[v + 32 * u], ev, expmax));
+          if (v + 32 * u < nvec) __stcs(drow + v + 32 * u, Upd<T>::apply(cur[u], xb[v + 32 * u], ev, p.eta, expmax));
       }
     }
 
@@ -552,7 +558,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
     float ev = 0.f;
     uint4 *drow = nullptr;
     if (FUSE) {
-      ev = p.eta * E::to_f(static_cast<const __nv_bfloat16 *>(p.Vt)[(size_t)p.v_row[m] * dm + i]);
+      ev = E::to_f(static_cast<const __nv_bfloat16 *>(p.Vt)[(size_t)p.v_row[m] * dm + i]);
       drow = s_dst0[m] + (size_t)i * nvec;
     }
     for (int v0 = lane; v0 < nvec; v0 += 32 * kDU) {
@@ -571,7 +577,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
       if (FUSE) {
 #pragma unroll
         for (int u = 0; u < kDU; ++u)
-          if (v0 + 32 * u < nvec) __stcs(drow + v0 + 32 * u, Upd<__nv_bfloat16>::apply(w[u], xb[v0 + 32 * u], ev, expmax));
+          if (v0 + 32 * u < nvec) __stcs(drow + v0 + 32 * u, Upd<__nv_bfloat16>::apply(w[u], xb[v0 + 32 * u], ev, p.eta, expmax));
       }
     }
     float sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);

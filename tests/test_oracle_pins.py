@@ -126,8 +126,9 @@ def test_write_bf16_storage_is_library_rounding_of_exact_candidate():
     exact = S + eta * (V.T @ Z)                     # exact in fp64 at these sizes? check via fp32 path
     ref = torch.from_numpy(exact.astype(np.float32)).to(torch.bfloat16).double().numpy()
     got = nm.boundary_update(S, Z, V, eta, "bf16")
-    # rounding fp64 directly vs fp64->fp32->bf16 can differ only on double-rounding ties
-    assert np.mean(got == ref) > 0.99 and nm.normwise_rel_err(got, exact) < 2 ** -8
+    # reading xi: the storage RNE rounds the fp32 accumulator value -> exactly torch's
+    # fp64 -> fp32 -> bf16 conversion (library routines)
+    assert np.array_equal(got, ref) and nm.normwise_rel_err(got, exact) < 2 ** -8
 
 
 def test_committed_state_closed_form_chunking_invariance():
