@@ -24,48 +24,12 @@
 // device copy used when a pinned checkpoint slot must be preserved, for
 // fork, and for rollback from the checkpoint pool.
 #include "../internal.h"
+#include "commit.cuh"
 
 namespace ttt {
 namespace {
 
-__global__ void commit_kernel(const CommitParams p) {
-  int bad_any = 0;
-  for (int b = threadIdx.x; b < p.n; b += blockDim.x) {
-    const int o = p.owner_idx[b];
-    const int bad = *reinterpret_cast<volatile int *>(p.mfail + o);
-    if (p.forced_fail) {                         // injected: the host runs the singleton retries
-      // (the flag stays: a fused C = 1 candidate is not recomputed by its retry; rollback /
-      // alloc / fork clear it through set_state_kernel)
-      if (p.partial && !((p.fail_bits[b / 32] >> (b % 32)) & 1u)) {   // test hook (negative control)
-        p.sel[o] ^= 1;
-        p.version[o] += 1ull;
-      }
-      continue;
-    }
-    p.mfail[o] = 0;                              // resolved here; the next WRITE raises it again if it must
-    if (!bad) {
-      p.sel[o] ^= 1;
-      p.version[o] += 1ull;
-    } else {
-      const int k = atomicAdd(p.rlog_count, 1);
-      RefusalRec r;
-      r.owner = p.owner_id[b];
-      r.version = p.version[o];
-      r.seq = p.seq;
-      r.pad = 0;
-      p.rlog[k % kRefusalLog] = r;
-    }
-    bad_any |= bad;
-    HostOwnerState h;
-    h.version = p.version[o];
-    h.seq = p.seq;
-    h.sel = p.sel[o];
-    h.pad = 0;
-    p.hstate[o] = h;                             // posted writes into mapped host memory
-  }
-  if (__syncthreads_or(bad_any) && threadIdx.x == 0) atomicAdd(p.fail_count, 1);
-  __threadfence_system();
-}
+__global__ void commit_kernel(const CommitParams p) { commit_members(p); }
 
 __global__ void copy_kernel(uint4 *__restrict__ dst, const uint4 *__restrict__ src, size_t n16) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;

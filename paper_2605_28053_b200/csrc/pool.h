@@ -76,5 +76,6 @@ struct ttt_pool {
   int *d_fail_count() const { return reinterpret_cast<int *>(arena + lay.flags); }
   int *d_rlog_count() const { return reinterpret_cast<int *>(arena + lay.flags + 16); }
   int *d_mfail() const { return reinterpret_cast<int *>(arena + lay.mfail); }
+  int *d_wctr() const { return reinterpret_cast<int *>(arena + lay.flags + 32); }   // fused-commit arrivals
   ttt::RefusalRec *d_rlog() const { return reinterpret_cast<ttt::RefusalRec *>(arena + lay.rlog); }
 };

@@ -677,6 +677,26 @@ ttt_status write_commit_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerR
   if (fail_mask)
     for (int b = 0; b < g->n; ++b) forced |= (fail_mask[b / 32] >> (b % 32)) & 1u;
   if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
+  CommitParams cp{};
+  cp.sel = p->d_sel();
+  cp.version = p->d_ver();
+  cp.mfail = p->d_mfail();
+  cp.fail_count = p->d_fail_count();
+  cp.rlog_count = p->d_rlog_count();
+  cp.rlog = p->d_rlog();
+  cp.hstate = p->hstate_dev;
+  cp.seq = forced ? 0 : p->commit_seq + 1;
+  cp.forced_fail = forced ? 1 : 0;
+  cp.n = g->n;
+  for (int b = 0; b < g->n; ++b) {
+    cp.owner_idx[b] = recs[b]->idx;
+    cp.owner_id[b] = g->owner_map[b];
+  }
+  const bool partial = forced && (g_test_hook.load() & TTT_HOOK_NO_GROUP_ATOMICITY);
+  cp.partial = partial ? 1 : 0;
+  if (partial)
+    for (int b = 0; b < g->n; ++b) cp.fail_bits[b / 32] = fail_mask[b / 32];
+  bool committed = false;                           // commit fused into the WRITE kernel
   if (!fused && sh.backend == TTT_LOW_RANK) {
     for (int b = 0; b < g->n; ++b)
       if (pinned_in_shadow(*recs[b])) CUDA_TRY(evict_pinned(p, *recs[b], s));
@@ -711,34 +731,21 @@ ttt_status write_commit_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerR
     wp.n = g->n; wp.d_model = sh.d_model; wp.d_ff = sh.d_ff; wp.C = sh.chunk;
     wp.max_owners = p->max_owners; wp.max_slots = 2 * p->max_owners + p->n_ckpt;
     for (int b = 0; b < g->n; ++b) wp.owner_idx[b] = recs[b]->idx;
-    for (int l = 0; l < sh.n_layers; ++l) {
-      wp.layer_off = (long long)l * p->E;
-      wp.tz_layer = (long long)l * sh.chunk * sh.d_ff;
-      wp.tv_layer = (long long)l * sh.chunk * sh.d_model;
-      cudaError_t e = use_tc ? launch_write_tc(wp, s) : launch_write_simt(sh.dtype, wp, s);
+    if (use_tc) {                                   // every layer in one launch, commit fused
+      cudaError_t e = launch_write_tc(wp, &cp, p->d_wctr(), s);
       if (e != cudaSuccess) return cuda_fail(e, "write launch");
+      committed = true;
+    } else {
+      for (int l = 0; l < sh.n_layers; ++l) {
+        wp.layer_off = (long long)l * p->E;
+        wp.tz_layer = (long long)l * sh.chunk * sh.d_ff;
+        wp.tv_layer = (long long)l * sh.chunk * sh.d_model;
+        cudaError_t e = launch_write_simt(sh.dtype, wp, s);
+        if (e != cudaSuccess) return cuda_fail(e, "write launch");
+      }
     }
   }
-  CommitParams cp{};
-  cp.sel = p->d_sel();
-  cp.version = p->d_ver();
-  cp.mfail = p->d_mfail();
-  cp.fail_count = p->d_fail_count();
-  cp.rlog_count = p->d_rlog_count();
-  cp.rlog = p->d_rlog();
-  cp.hstate = p->hstate_dev;
-  cp.seq = forced ? 0 : p->commit_seq + 1;
-  cp.forced_fail = forced ? 1 : 0;
-  cp.n = g->n;
-  for (int b = 0; b < g->n; ++b) {
-    cp.owner_idx[b] = recs[b]->idx;
-    cp.owner_id[b] = g->owner_map[b];
-  }
-  const bool partial = forced && (g_test_hook.load() & TTT_HOOK_NO_GROUP_ATOMICITY);
-  cp.partial = partial ? 1 : 0;
-  if (partial)
-    for (int b = 0; b < g->n; ++b) cp.fail_bits[b / 32] = fail_mask[b / 32];
-  CUDA_TRY(launch_commit(cp, s));
+  if (!committed) CUDA_TRY(launch_commit(cp, s));
   if (partial)                                    // the broken contract the negative control needs
     for (int b = 0; b < g->n; ++b) {
       if ((fail_mask[b / 32] >> (b % 32)) & 1u) continue;
