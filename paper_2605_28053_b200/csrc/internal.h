@@ -152,7 +152,7 @@ int read_decode_mma_chunks(int dtype, int d_ff);   // > 0: the bf16 tensor-core-
 cudaError_t launch_write_simt(int dtype, const WriteParams &p, cudaStream_t s);
 // bf16, tcgen05: every layer in one launch; cp != nullptr fuses the group commit (last CTA, `arrive`)
 cudaError_t launch_write_tc(const WriteParams &p, const CommitParams *cp, int *arrive, cudaStream_t s);
-bool write_tc_supported(int d_model, int d_ff, int C);
+bool write_tc_supported(int d_model, int d_ff, int C, int n_layers);
 cudaError_t launch_commit(const CommitParams &p, cudaStream_t s);
 cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s);
 cudaError_t launch_set_state(int *sel, unsigned long long *version, int *mfail, int idx, int sel_v,

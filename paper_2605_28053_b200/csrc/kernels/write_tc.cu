@@ -55,6 +55,8 @@ constexpr int BM = 128;
 constexpr int kEpiThreads = 256;                 // 8 epilogue warps: 2 per TMEM lane quarter
 constexpr int kThreads = 64 + kEpiThreads;      // producer warp, MMA warp, 8 epilogue warps
 constexpr int kBox = BM * 128;                    // one 128-row x 64-column bf16 box (16 KB)
+constexpr int kMaxLayers = 40;                    // segment table in shared memory (BN = 256, C = 128 fills 227 KB)
+constexpr int kMaxSeg = 2 * kMaxLayers + 1;
 
 struct TcParams {
   int n, d_model, d_ff, C, L;
@@ -107,26 +109,56 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mb = p.d_model / BM, nb = p.d_ff / BN;
   const int per_member = mb * nb, per_layer = p.n * per_member;
-  // Layer-synchronous partition: in every layer this CTA takes the same contiguous range
-  // [a, b) of that layer's (member, j-block, i-block) tiles, so at any time the 148 CTAs
-  // stream neighbouring column blocks of the same ΔW rows (DRAM page locality), and the
-  // pipeline runs on from one layer into the next without a launch boundary.
-  const int a = (int)((long long)per_layer * blockIdx.x / gridDim.x);
-  const int cnt = (int)((long long)per_layer * (blockIdx.x + 1) / gridDim.x) - a;
-  const int t0 = 0, t1 = cnt * p.L;               // local tile sequence of this CTA
-  auto tile_of = [&](int t) {
+  // Layer-synchronous partition: in every layer each CTA takes the same number q = ⌊T_l / G⌋ of
+  // contiguous tiles, [q·bid, q·bid + q), so the CTAs stay in lockstep and at any time stream
+  // neighbouring column blocks of the same ΔW rows (DRAM page locality: a per-layer launch order
+  // measured 5.08 ms, a CTA-contiguous order over all layers 6.35 ms); the pipeline runs on from
+  // one layer into the next without a launch boundary.  The T_l − q·G leftover tiles of every
+  // layer are dealt round-robin over the CTAs after the last layer (balanced within one tile).
+  // Segment table (shared memory): seg[i] = first local index of segment i, seg_l / seg_a =
+  // its layer and first tile in that layer.
+  int *seg = reinterpret_cast<int *>(last_flag + 2), *seg_l = seg + kMaxSeg + 1, *seg_a = seg_l + kMaxSeg;
+  int &n_seg = last_flag[1];
+  if (threadIdx.x == 0) {
+    const int q = per_layer / gridDim.x, rem = per_layer - q * gridDim.x;
+    int acc = 0, ns = 0;
+    for (int l = 0; l < p.L && q > 0; ++l, ++ns) {
+      seg[ns] = acc;
+      seg_l[ns] = l;
+      seg_a[ns] = q * blockIdx.x;
+      acc += q;
+    }
+    for (int j = blockIdx.x; j < p.L * rem; j += gridDim.x, ++ns) {   // leftovers, one tile each
+      seg[ns] = acc;
+      seg_l[ns] = j / rem;
+      seg_a[ns] = q * gridDim.x + j % rem;
+      acc += 1;
+    }
+    seg[ns] = acc;
+    n_seg = ns;
+  }
+  __syncthreads();
+  const int t0 = 0, t1 = seg[n_seg];              // local tile sequence of this CTA
+  // Each role walks its tiles in order with a segment cursor (a scan per tile would put a
+  // chain of dependent shared-memory loads on the single producer / MMA threads).
+  auto seg_of = [&](int t, int &cur) {
+    while (t >= seg[cur + 1]) ++cur;
+    return cur;
+  };
+  auto tile_of = [&](int t, int &cur) {
+    const int i = seg_of(t, cur);
     Tile r;
-    r.l = t / cnt;
-    int rem = a + (t - r.l * cnt);
+    r.l = seg_l[i];
+    int rem = seg_a[i] + (t - seg[i]);
     r.b = rem / per_member;
     rem -= r.b * per_member;
     r.jb = rem / mb;
     r.ib = rem - r.jb * mb;
     return r;
   };
-  auto strip_of = [&](int t) {                    // (layer, member, j-block): B stays resident
-    const int l = t / cnt;
-    return l * (per_layer / mb) + (a + (t - l * cnt)) / mb;
+  auto strip_of = [&](int t, int &cur) {          // (layer, member, j-block): B stays resident
+    const int i = seg_of(t, cur);
+    return seg_l[i] * (per_layer / mb) + (seg_a[i] + (t - seg[i])) / mb;
   };
 
   if (threadIdx.x == 0) {
@@ -163,12 +195,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ΔW_v is read once: evict_first; the tail tiles are re-read by the ~18 CTAs on the same
       // member (V_c once per tile): evict_last (ncu r2: 11 % extra DRAM reads without hints)
       const u64 pol_stream = (HINT & 2) ? policy_evict_first() : 0, pol_keep = (HINT & 1) ? policy_evict_last() : 0;
-      int k = 0, kb = 0, strip = -1, nstrip = 0;
+      int k = 0, kb = 0, strip = -1, nstrip = 0, cur = 0;
       for (int t = t0; t < t1; ++t, ++k) {
-        const Tile tl = tile_of(t);
+        const Tile tl = tile_of(t, cur);
         const int o = p.owner_idx[tl.b];
         const int tail_idx = o * p.L + tl.l;
-        if (strip_of(t) != strip) {               // new (layer, member, j-block): reload the resident Z_c tile
+        const int sid = strip_of(t, cur);
+        if (sid != strip) {                       // new (layer, member, j-block): reload the resident Z_c tile
           if (nstrip > 0) mbar_wait(b_empty, (nstrip - 1) & 1);
           mbar_expect_tx(b_full, b_bytes);
           for (int h = 0; h < kHB; ++h)
@@ -176,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_3d_hint(sB + h * (C * 128), &tmZ, b_full, tl.jb * BN + 64 * h, 0, tail_idx, pol_keep);
             else
               tma_load_3d(sB + h * (C * 128), &tmZ, b_full, tl.jb * BN + 64 * h, 0, tail_idx);
-          strip = strip_of(t);
+          strip = sid;
           ++nstrip;
         }
         const int s = k & 1;
@@ -204,11 +237,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc = idesc_bf16(BM, BN, 1, 1);   // A = V_c, B = Z_c, both MN-major
-    int k = 0, strip = -1, nstrip = 0;
+    int k = 0, strip = -1, nstrip = 0, cur = 0;
     for (int t = t0; t < t1; ++t, ++k) {
-      if (strip_of(t) != strip) {
+      const int sid = strip_of(t, cur);
+      if (sid != strip) {
         mbar_wait(b_full, nstrip & 1);
-        strip = strip_of(t);
+        strip = sid;
         ++nstrip;
       }
       const int s = k & 1, acc = k & 1;
@@ -226,7 +260,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(a_empty + s);                  // A stage free once these MMAs retire
         mma_commit(t_full + acc);                 // accumulator ready for the epilogue
-        if (t + 1 >= t1 || strip_of(t + 1) != strip) mma_commit(b_empty);
+        int nxt = cur;
+        if (t + 1 >= t1 || strip_of(t + 1, nxt) != strip) mma_commit(b_empty);
       }
       __syncwarp();
     }
@@ -238,9 +273,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int et = threadIdx.x - 64;
     uint32_t expmax = 0;                          // max exponent field seen (non-finite guard)
     const u64 eta2 = pack_u2(__float_as_uint(p.eta), __float_as_uint(p.eta));
-    int k = 0, kb = 0;
+    int k = 0, kb = 0, cur = 0;
     for (int t = t0; t < t1; ++t, ++k) {
-      const Tile tl = tile_of(t);
+      const Tile tl = tile_of(t, cur);
       const int acc = k & 1;
       mbar_wait(t_full + acc, (k >> 1) & 1);
       tc_fence_after();
@@ -333,7 +368,7 @@ int write_cfg(int d_ff) {
 }
 
 size_t smem_bytes(int C, const Cfg &k) {
-  return 1024 + 2 * (size_t)C * BM * 2 + (size_t)C * k.BN * 2 + (size_t)k.SB * kBox + 512;
+  return 1024 + 2 * (size_t)C * BM * 2 + (size_t)C * k.BN * 2 + (size_t)k.SB * kBox + 256 + 12 * (kMaxSeg + 1);
 }
 
 // Tensor maps depend only on the pool's arena regions and shape: encoded once per pool.
@@ -395,9 +430,9 @@ cudaError_t launch_cfg(const Maps &m, const TcParams &p, int tiles, size_t smem,
 
 }  // namespace
 
-bool write_tc_supported(int d_model, int d_ff, int C) {
+bool write_tc_supported(int d_model, int d_ff, int C, int n_layers) {
   const Cfg &k = kCfgs[write_cfg(d_ff)];
-  return d_model % BM == 0 && d_ff % k.BN == 0 && C % 16 == 0 && C >= 16 && C <= 128 &&
+  return n_layers <= kMaxLayers && d_model % BM == 0 && d_ff % k.BN == 0 && C % 16 == 0 && C >= 16 && C <= 128 &&
          smem_bytes(C, k) <= 227 * 1024 && encode_fn() != nullptr;
 }
 

@@ -671,7 +671,7 @@ ttt_status write_commit_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerR
   if (!fused && need_evict > (int)p->free_ckpt.size())
     return fail(TTT_E_POOL_FULL, "no free checkpoint slot for a pinned snapshot");
   const int impl = g_write_impl.load();
-  const bool use_tc = sh.dtype == TTT_BF16 && impl != 1 && write_tc_supported(sh.d_model, sh.d_ff, sh.chunk);
+  const bool use_tc = sh.dtype == TTT_BF16 && impl != 1 && write_tc_supported(sh.d_model, sh.d_ff, sh.chunk, sh.n_layers);
   if (!fused && impl == 2 && !use_tc) return fail(TTT_E_SHAPE, "tcgen05 WRITE kernel does not support this shape");
   bool forced = false;
   if (fail_mask)
