@@ -31,12 +31,19 @@ namespace {
 
 __global__ void commit_kernel(const CommitParams p) { commit_members(p); }
 
-__global__ void copy_kernel(uint4 *__restrict__ dst, const uint4 *__restrict__ src, size_t n16) {
+// K5 (HBM-bound, 2 x slot bytes): 8 independent 16-B streaming loads per thread in flight
+// (128 B x 2048 threads = 256 KB per SM), then 8 streaming stores; neither side is re-read soon.
+__global__ void __launch_bounds__(512) copy_kernel(uint4 *__restrict__ dst, const uint4 *__restrict__ src,
+                                                   size_t n16) {
+  constexpr int U = 8;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < n16; i += 4 * stride) {
-    uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
-    dst[i] = a; dst[i + stride] = b; dst[i + 2 * stride] = c; dst[i + 3 * stride] = d;
+  for (; i + (U - 1) * stride < n16; i += U * stride) {
+    uint4 v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) v[k] = __ldcs(src + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < U; ++k) __stcs(dst + i + k * stride, v[k]);
   }
   for (; i < n16; i += stride) dst[i] = src[i];
 }

@@ -40,7 +40,7 @@ def main():
     W = torch.empty(L, dm, dff, dtype=torch.bfloat16, device=dev)
     for l in range(L):
         capi.gen_uniform(W[l], 0, rng.T_W_DOWN, 0, l, 0, dm * dff, rng.amp_inv_sqrt(dff), True)
-    eng = Engine(dm, dff, C, L, "bf16", B, W, n_ckpt=0, B=B)
+    eng = Engine(dm, dff, C, L, "bf16", B + 1, W, n_ckpt=0, B=B)   # +1 owner slot: the fork / K5 copy target
     owners = list(range(100, 100 + B))
     d0 = torch.empty(L, dm, dff, dtype=torch.bfloat16, device=dev)
     for o in owners:
@@ -101,6 +101,24 @@ def main():
     wbytes = B * (2 * dm * dff * 2 + C * (dff + dm) * 2)
     res["write"] = {"ms_per_layer": wms, "GBps": wbytes / wms / 1e6, "frac_hbm": wbytes / wms / 1e6 / hbm,
                     "alg_bytes": wbytes, "impl": a.write_impl}
+    # K5 checkpoint copy (copy_kernel; App. G "Checkpoint write"): the committed slot of
+    # one owner (L layers of ΔW) copied into another slot — the same kernel a pinned checkpoint's
+    # eviction, a fork and a rollback-from-pool run.  Timed through tttstate_fork (copy + one
+    # 1-thread set_state launch); bytes = read + write of the slot.
+    cms = []
+    for i in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        capi.tttstate_fork(eng.pool, owners[0], 99999, s)
+        e1.record(s)
+        torch.cuda.synchronize()
+        capi.tttstate_free(eng.pool, 99999)
+        cms.append(e0.elapsed_time(e1))
+    cms = sorted(cms[1:])
+    cbytes = 2 * L * dm * dff * 2
+    res["checkpoint_copy"] = {"ms": cms[len(cms) // 2], "GBps": cbytes / cms[len(cms) // 2] / 1e6,
+                              "frac_hbm": cbytes / cms[len(cms) // 2] / 1e6 / hbm, "alg_bytes": cbytes,
+                              "kernel": "copy_kernel (16-B vector grid-stride copy, 4 x SMs CTAs of 512)"}
     print(json.dumps(res, indent=1))
 
 
