@@ -411,16 +411,16 @@ def main():
     n_launch0 = capi.tttstate_launch_count()
     plan0, census0 = srv.plan_s, dict(srv.log.census)
     nplan0 = len(srv.log.plan)
-    wall0 = time.perf_counter()
     with ClockSampler(local) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        wall0 = time.perf_counter()                 # host wall of the timed region (sampler start/stop excluded)
         e0.record(stream)
         for _ in range(a.steps):
             run_window()
         e1.record(stream)
         torch.cuda.synchronize(dev)
+        wall_s = time.perf_counter() - wall0
     n_launch = capi.tttstate_launch_count() - n_launch0
-    wall_s = time.perf_counter() - wall0
     plan_s = srv.plan_s - plan0
     census = {("READ" if k == 0 else "WRITE"): v - census0.get(k, 0) for k, v in srv.log.census.items()}
     # group-size and wait (issue − ready, Eq. 4) histograms of the timed region's plan log
