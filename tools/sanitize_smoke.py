@@ -43,4 +43,11 @@ Y = torch.empty(2, 16, 256, device="cuda", dtype=torch.bfloat16)
 capi.read_apply_chunk(eng.pool, g, 0, X, X, Y)
 capi.write_commit(eng.pool, g, 0.01)
 torch.cuda.synchronize()
+# r2: one-launch tcgen05 WRITE with the fused commit (BN = 256 and 128 tile paths) and the
+# device-side App. H resolution (a poisoned member refused, the others published), through
+# the native serving step
+for dff in (512, 384):
+    run(T.uniform_small(n_streams=4, n_layers=2, d_model=256, d_ff=dff, chunk=16, n_steps=34, dtype="bf16",
+                        delta0="rng", controls={(1, 15): ["poison"], (2, 20): ["snapshot"], (2, 33): ["rollback"],
+                                                (3, 31): ["fail"]}), impl=2)
 print("sanitize smoke ok")
