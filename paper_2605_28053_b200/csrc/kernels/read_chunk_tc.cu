@@ -20,6 +20,8 @@
 //    swizzle), warp 1 TMEM alloc + single-thread MMA issue, warps 2-5
 //    epilogue (tcgen05.ld → bf16 → Y); during the mainloop the epilogue warps
 //    of each of a member's N-tiles append 1/nt of the chunk to the tail.
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "../internal.h"
@@ -69,6 +71,7 @@ struct ChunkParams {
   long long y32_slab;
   int x_rowmap;                  // X map is [rows][d_ff]: row block b starts at row 128·b
   int cooperative;               // LR: launch cooperatively (co-residency guaranteed)
+  int trace;                     // LR: TTT_LR_PRINT=1 prints per-CTA %globaltimer phase stamps (profiling)
   int owner_idx[kMaxGroup];
   LrFused lr;
 };
@@ -176,6 +179,15 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = p.nt, nk_all = p.d_ff / BK, KS = p.ksplit;
+  __shared__ unsigned long long ts[8];              // LR profiling stamps (p.trace)
+  auto stamp = [&](int i) {
+    if (LR && p.trace) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[i] = t;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
   auto n0_of = [&](int j) { return j < p.h ? j * p.w_hi : p.h * p.w_hi + (j - p.h) * (p.w_hi - 16); };
   auto width_of = [&](int j) { return j < p.h ? p.w_hi : p.w_hi - 16; };
   const int n_tiles = p.n * nt * KS;
@@ -225,6 +237,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
     }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) stamp(1);
 
   if (warp == 0) {
     if (lane == 0) {                                        // ---------------- TMA producer
@@ -274,6 +287,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
         __syncwarp();
       }
     }
+    if (lane == 0) stamp(2);                                // last MMA issued
   } else if (warp < 6) {                                    // ---------------- epilogue warps 2-5
     const int q = warp & 3, row = q * 32 + lane;            // token index t in the chunk
     const int et = threadIdx.x - 64;
@@ -333,6 +347,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
       if (lane == 0) mbar_arrive(t_empty);
       if (LR) {                                    // f1: arm the finish of this tile
         named_bar<1, 128>();                       // this CTA's slab is written
+        if (et == 0) stamp(3);
         if (et == 0) {
           int *tick = p.lr.ctr + 2 + b * nt + j;
           __threadfence();
@@ -340,6 +355,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
           while (ld_volatile(tick) < KS) __nanosleep(64);            // every K slab of the tile
           while (ld_volatile(p.lr.ctr) < p.valid_rows) __nanosleep(64);   // every member's Bᵀu
           __threadfence();
+          stamp(6);
         }
         lr_finish<BN>(p, b, j, ks, n0, width, et);   // with the u warps (named barrier 2)
       }
@@ -394,6 +410,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
         if (lane == 0) us_lr[k] = sum;
       }
       named_bar<3, 32 * kUW>();   // u_m complete (shared memory)
+      if (ut == 0) stamp(4);
       // Bᵀu_m: 8 outputs per thread, the R rows of B_m streamed 8 loads at a time
       const uint4 *B4 = reinterpret_cast<const uint4 *>(A + (size_t)R * dff);
       for (int i8 = ut; i8 < dm / 8; i8 += 32 * kUW) {
@@ -421,6 +438,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
         o4[1] = make_float4(y[4], y[5], y[6], y[7]);
       }
       named_bar<3, 32 * kUW>();   // Bᵀu_m written
+      if (ut == 0) stamp(5);
       if (ut == 0) {
         __threadfence();
         atomicAdd(lr.ctr, 1);
@@ -434,6 +452,11 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
   __syncwarp();                                    // warp 0: the producer lane rejoins its warp
   __syncthreads();
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
+  if (LR && p.trace && threadIdx.x == 0) {
+    stamp(7);
+    printf("LRT %d %llu %llu %llu %llu %llu %llu %llu %llu\n", (int)blockIdx.x, ts[0], ts[1], ts[2], ts[3], ts[4],
+           ts[5], ts[6], ts[7]);
+  }
   if (LR && threadIdx.x == 0) {                    // the last CTA out re-arms the counters
     __threadfence();
     if (atomicAdd(p.lr.ctr + 1, 1) == (int)gridDim.x - 1) {
@@ -577,6 +600,8 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
   p.y32_slab = cl.y32_slab;
   p.x_rowmap = cl.x_rowmap;
   p.cooperative = cl.cooperative;
+  static const int lr_print = getenv("TTT_LR_PRINT") ? atoi(getenv("TTT_LR_PRINT")) : 0;
+  p.trace = lr_print;
   for (int b = 0; b < cl.n; ++b) p.owner_idx[b] = cl.owner_idx[b];
   const int sms = device_sm_count();
   const NPlan np = plan_n(cl.d_model, cl.n * std::max(1, cl.ksplit), sms);
