@@ -320,11 +320,30 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
       __nv_bfloat16 *yrow = static_cast<__nv_bfloat16 *>(p.Y) + ((size_t)b * p.C + row) * p.d_model + n0;
       float *yrow32 = p.Y32 ? p.Y32 + ks * p.y32_slab + ((size_t)b * p.C + row) * p.d_model + n0 : nullptr;
       const bool valid = row < p.C && (!p.Y32 || b * p.C + row < p.valid_rows);
+      // f1 split-K slab (fp32): each lane's tcgen05.ld row is transposed through shared memory
+      // (the TMA ring is idle once the single tile's MMAs retired) so a warp store writes 8 rows ×
+      // 64 contiguous bytes instead of 32 rows × 16 bytes (trace r2: this epilogue took 3.5 µs, now
+      // 2.1; R = 16 31.6 -> 29.4 µs per layer, R = 64 56.3 -> 54.2; 32-column steps measured 30.8 µs)
+      float *stg = LR ? reinterpret_cast<float *>(smem) + q * (32 * 17) : nullptr;
 #pragma unroll 1
       for (int c = 0; c < width / 16; ++c) {      // 16 accumulator columns at a time
         uint32_t r[16];
         tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 16), r);
-        if (valid && yrow32) {
+        if (LR && yrow32) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) stg[lane * 17 + e] = __uint_as_float(r[e]);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = i * 8 + (lane >> 2), c4 = (lane & 3) * 4, grow = b * p.C + q * 32 + rr;
+            if (q * 32 + rr < p.C && grow < p.valid_rows) {
+              const float *sp = stg + rr * 17 + c4;
+              *reinterpret_cast<float4 *>(p.Y32 + ks * p.y32_slab + (size_t)grow * p.d_model + n0 + c * 16 + c4) =
+                  make_float4(sp[0], sp[1], sp[2], sp[3]);
+            }
+          }
+          __syncwarp();
+        } else if (valid && yrow32) {
           float4 *d4 = reinterpret_cast<float4 *>(yrow32 + c * 16);
 #pragma unroll
           for (int v = 0; v < 4; ++v)
