@@ -39,6 +39,7 @@ struct ReadParams {
   int dyn;                       // per-CTA dynamic task hand-out (SM-interleaved order only)
   int kc;                        // > 0: tensor-core base (bf16), Pbase holds kc K-chunk slabs [kc][8][d_model]
   int l2keep;                    // not the group's last launch of this layer: keep W_down in L2 (evict_last)
+  int xtma;                      // tensor-core-base kernel: stage the x rows with bulk copies (TMA)
 };
 
 // a5: chunk update of one layer for every member (shadow slot <- ΔW_v + η VᵀZ).

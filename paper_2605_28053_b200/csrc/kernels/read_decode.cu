@@ -367,6 +367,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
   __shared__ const uint4 *s_row0[kMaxReadMembers + 1];
   __shared__ uint4 *s_dst0[kMaxReadMembers];
   __shared__ int s_next;                                  // per-CTA dynamic task counter (p.dyn)
+  __shared__ __align__(8) unsigned long long s_xbar;      // p.xtma: x rows staged by bulk copies
 
   const int n = p.n, dff = p.d_ff, dm = p.d_model, nvec = dff / 8, nvp = mma_nvp(nvec);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, tq = lane & 3;
@@ -409,11 +410,24 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
 
   uint4 cur[4], nxt[4];
   const bool early = t < n_base;                  // base tasks read only W_down before the wait
+  if (p.xtma && tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_xbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (early) load_base(cur, t, 0);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (tid <= n) {
     if (tid == 0) {
       s_row0[0] = W;
+      if (p.xtma) {                               // the n x rows: one bulk copy each (no registers)
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_xbar), bytes = (uint32_t)dff * 2;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * n) : "memory");
+        for (int b = 0; b < n; ++b)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(xs + (size_t)b * nvp)),
+                       "l"(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff), "r"(bytes), "r"(bar)
+                       : "memory");
+      }
     } else {
       const int o = p.owner_idx[tid - 1];
       s_row0[tid] = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.slots) +
@@ -431,8 +445,15 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
     row = s_row0[m + 1] + (size_t)(td - m * dm) * nvec;
     load_delta(cur, row, v);
   }
-  // x rows (zero pad / absent members): kXStage loads per thread in flight, then the stores
-  for (int base = tid; base < kMaxReadMembers * nvp; base += kXStage * kMmaThreads) {
+  // x rows (zero pad / absent members): kXStage loads per thread in flight, then the stores;
+  // p.xtma: only the zero padding here, the rows arrive by bulk copy
+  if (p.xtma) {
+    for (int idx = tid; idx < kMaxReadMembers * nvp; idx += kMmaThreads) {
+      const int b = idx / nvp, vv = idx - b * nvp;
+      if (b >= n || vv >= nvec) xs[idx] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  for (int base = p.xtma ? kMaxReadMembers * nvp : tid; base < kMaxReadMembers * nvp; base += kXStage * kMmaThreads) {
     uint4 tmp[kXStage];
 #pragma unroll
     for (int e = 0; e < kXStage; ++e) {
@@ -459,6 +480,10 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
           (static_cast<const __nv_bfloat16 *>(p.Vt) + (size_t)p.v_row[b] * dm)[ii];
     }
   }
+  if (p.xtma)                                     // every thread observes the bulk copies' completion
+    asm volatile("{\n\t.reg .pred P;\nXW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t@!P bra XW_%=;\n}" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_xbar))
+                 : "memory");
   __syncthreads();
   if (t >= n_tasks) return;
 
@@ -694,9 +719,11 @@ cudaError_t launch_mma(const ReadParams &p, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  static const int xtma = getenv("TTT_READ_XTMA") ? atoi(getenv("TTT_READ_XTMA")) : 1;
   ReadParams q = p;
   q.order = order;
   q.dyn = order == 1 ? dyn : 0;
+  q.xtma = xtma;
   cudaError_t e = cudaLaunchKernelEx(&cfg, read_decode_mma_kernel<FUSE, L2H>, q);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
