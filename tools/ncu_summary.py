@@ -52,7 +52,8 @@ def summarise(rep, label, outdir):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         rdb = rd * scale.get(u["dram__bytes_read.sum"], 1)
         wrb = wr * scale.get(u["dram__bytes_write.sum"], 1)
-        t_ns = float(d["gpu__time_duration.sum"]) * (1e3 if u["gpu__time_duration.sum"] == "us" else 1)
+        tscale = {"ns": 1, "nsecond": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}
+        t_ns = float(d["gpu__time_duration.sum"]) * tscale.get(u["gpu__time_duration.sum"], 1)
         lines.append(f"# dram traffic per launch = {rdb + wrb:.4e} B; achieved {(rdb + wrb) / t_ns:.1f} GB/s "
                      f"(cold-cache, serialised replay)")
         all_lines += lines + [""]
@@ -62,14 +63,15 @@ def summarise(rep, label, outdir):
     return res
 
 
-def shares(launches, outdir, read_per_window=127 * 36 + 36, write_per_window=36):
+def shares(launches, outdir, read_per_window=127 * 36 + 36, write_per_window=1):   # r2: one WRITE launch (all layers)
     lines_in = [l for l in open(launches) if not l.startswith("==")]
     rows = list(csv.DictReader(io.StringIO("".join(lines_in))))
     per = defaultdict(list)
     for r in rows:
         if r.get("Metric Name") == "gpu__time_duration.sum":
             name = r["Kernel Name"].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
-            per[name].append(float(r["Metric Value"]))
+            unit = r.get("Metric Unit", "nsecond")
+            per[name].append(float(r["Metric Value"]) * {"usecond": 1e3, "msecond": 1e6}.get(unit, 1))
     lines = ["# per-kernel launch times from the ncu launch list (cold-cache, serialised: compare SHARES)",
              "kernel, launches, mean_us"]
     means = {}
