@@ -358,7 +358,7 @@ constexpr int kDU = 4;                                  // ΔW loads per lane pe
 
 __host__ __device__ inline int mma_nvp(int nvec) { return (nvec + 127) / 128 * 128; }
 
-template <bool FUSE, bool L2H>
+template <bool FUSE, bool L2H, bool PRE1 = true>
 __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const ReadParams p) {
   constexpr int kWarps = kMmaThreads / 32;
   using E = Elem<__nv_bfloat16>;
@@ -480,6 +480,10 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
           (static_cast<const __nv_bfloat16 *>(p.Vt) + (size_t)p.v_row[b] * dm)[ii];
     }
   }
+  // base-first warps: the first task's second batch too, while the x rows are still arriving
+  // (the registers the LDG/STS x staging used are free with the bulk copies)
+  bool pre1 = PRE1 && p.xtma && early;
+  if (pre1) load_base(nxt, t, 1);
   if (p.xtma)                                     // every thread observes the bulk copies' completion
     asm volatile("{\n\t.reg .pred P;\nXW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t@!P bra XW_%=;\n}" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&s_xbar))
@@ -523,7 +527,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
     const uint4 *xg = xs + (size_t)g * nvp + kc * kMmaChunkVec + tq;
     float c[4] = {0.f, 0.f, 0.f, 0.f};
     for (int j = 0; j < nb; ++j) {
-      if (j + 1 < nb) load_base(nxt, t, j + 1);
+      if (j + 1 < nb && !(pre1 && j == 0)) load_base(nxt, t, j + 1);
       const uint4 b0 = xg[8 * j], b1 = xg[8 * j + 4];
       mma_bf16_16816(c, cur[0].x, cur[2].x, cur[0].y, cur[2].y, b0.x, b0.y);
       mma_bf16_16816(c, cur[0].z, cur[2].z, cur[0].w, cur[2].w, b0.z, b0.w);
@@ -532,6 +536,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
 #pragma unroll
       for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
     }
+    pre1 = false;
     const int nt = next_task(t);                  // prefetch the next task's first batch
     if (nt < n_base) load_base(cur, nt, 0);
     else if (nt < n_tasks) {
