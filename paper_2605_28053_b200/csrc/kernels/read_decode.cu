@@ -184,6 +184,12 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
   int v = lane;
   const uint4 *row = nullptr;
   const bool early = t < dm;                        // first task is a W_down row
+  __shared__ __align__(8) unsigned long long s_xbar;
+  const bool xtma = p.xtma && (reinterpret_cast<uintptr_t>(p.X) & 15) == 0;   // rows staged by bulk copies
+  if (xtma && tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_xbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (early) {
     row = static_cast<const uint4 *>(p.w_down_l) + (size_t)t * nvec;
     load(cur, row, v);
@@ -193,6 +199,15 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
   if (tid <= n) {
     if (tid == 0) {
       s_row0[0] = static_cast<const uint4 *>(p.w_down_l);
+      if (xtma) {                                  // the n x rows: one bulk copy each
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_xbar), bytes = (uint32_t)nvec * 16;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * n) : "memory");
+        for (int b = 0; b < n; ++b)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(xs + (size_t)b * nvec)),
+                       "l"(static_cast<const T *>(p.X) + (size_t)p.x_row[b] * dff), "r"(bytes), "r"(bar)
+                       : "memory");
+      }
     } else {
       const int o = p.owner_idx[tid - 1];
       const long long slot = 2LL * o + p.sel[o];
@@ -214,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
     load(cur, row, v);
   }
 
-  for (int idx = tid; idx < n * nvec; idx += kThreads) {
+  for (int idx = xtma ? n * nvec : tid; idx < n * nvec; idx += kThreads) {
     const int b = idx / nvec, vv = idx - b * nvec;
     xs[idx] = reinterpret_cast<const uint4 *>(static_cast<const T *>(p.X) + (size_t)p.x_row[b] * dff)[vv];
   }
@@ -233,6 +248,10 @@ __global__ void __launch_bounds__(kThreads, 1) read_decode_kernel(const ReadPara
           (static_cast<const T *>(p.Vt) + (size_t)p.v_row[b] * dm)[i];
     }
   }
+  if (xtma)                                        // every thread observes the bulk copies' completion
+    asm volatile("{\n\t.reg .pred P;\nXS_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t@!P bra XS_%=;\n}" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_xbar))
+                 : "memory");
   __syncthreads();
   if (t >= n_tasks) return;
   Acc acc[kMaxReadMembers];
@@ -657,8 +676,10 @@ cudaError_t launch_cfg1(const ReadParams &p, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   static const int order = getenv("TTT_READ_ORDER") ? atoi(getenv("TTT_READ_ORDER")) : 1;
+  static const int xtma = getenv("TTT_READ_XTMA") ? atoi(getenv("TTT_READ_XTMA")) : 1;
   ReadParams q = p;
   q.order = order;
+  q.xtma = xtma;
   cudaError_t e = cudaLaunchKernelEx(&cfg, read_decode_kernel<T, TH, U, FUSE>, q);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
