@@ -91,9 +91,11 @@ enum { TTT_FAST_WEIGHT = 0, TTT_LOW_RANK = 1, TTT_STREAMING = 2 }; /* τ */
 enum { TTT_MODE_SERIAL = 0, TTT_MODE_PHASE = 1, TTT_MODE_FULL = 2 };
 
 /* τ + σ of one pool.  rule 0: ΔW += η·V_cᵀZ_c (reading i).
+ * rule 1 (SPEC-compat, S:188 / S:215; fast-weight backend, d_model == d_ff):
+ * ΔW += η·m mᵀ with m the mean of the chunk's z; READ is unchanged, so the
+ * caller passes W_down = I to get SPEC's y = x + ΔW·x.
  * backend: TTT_FAST_WEIGHT (rank 0) or TTT_LOW_RANK (NEXT f1: payload A
- * [rank][d_ff] then B [rank][d_model] per layer, bf16, 1 <= rank <= 64).
- * Only rule 0 runs on the GPU.                                           */
+ * [rank][d_ff] then B [rank][d_model] per layer, bf16, 1 <= rank <= 64).  */
 typedef struct {
   int32_t backend, dtype, d_model, d_ff, chunk, rank, n_layers, rule;
 } ttt_shape;

@@ -151,6 +151,7 @@ cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s);
 bool read_decode_fits(int n, int d_model, int d_ff, int esize);
 int read_decode_mma_chunks(int dtype, int d_ff);   // > 0: the bf16 tensor-core-base READ applies (its K chunks)
 cudaError_t launch_write_simt(int dtype, const WriteParams &p, cudaStream_t s);
+cudaError_t launch_write_rule1(int dtype, const WriteParams &p, cudaStream_t s);   // SPEC-compat rule 1 (square)
 // bf16, tcgen05: every layer in one launch; cp != nullptr fuses the group commit (last CTA, `arrive`)
 cudaError_t launch_write_tc(const WriteParams &p, const CommitParams *cp, int *arrive, cudaStream_t s);
 bool write_tc_supported(int d_model, int d_ff, int C, int n_layers);

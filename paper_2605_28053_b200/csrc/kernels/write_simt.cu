@@ -16,6 +16,7 @@
 // in 32-token slices, fixed summation order t = 0..C−1.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "../internal.h"
@@ -106,7 +107,51 @@ __global__ void __launch_bounds__(NT) write_simt_kernel(const WriteParams p) {
   if (bad) atomicOr(p.mfail + o, 1);        // per-member flag: the commit resolves members
 }
 
+// SPEC-compat rule 1 (the CPU program's rank-1 stand-in, S:188 / S:206 / S:215; SURVEY §8(c)
+// step 7): m = (1/C) Σ_t z_t over the chunk's tail, ΔW̃ = ΔW_v + η·m mᵀ (square: d_model = d_ff;
+// the targets v_t are not used); READ is the unchanged y = (W_down + ΔW)·x with W_down = I.
+// One CTA row of the grid per member: every CTA recomputes m (C·d tail reads from L2) into
+// shared memory, then writes its share of the d×d candidate.
+template <typename T>
+__global__ void __launch_bounds__(256) write_rule1_kernel(const WriteParams p) {
+  extern __shared__ float m[];
+  const int b = blockIdx.y, o = p.owner_idx[b], d = p.d_ff;
+  const T *Z = static_cast<const T *>(p.tailZ) + o * p.tz_owner + p.tz_layer;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float s = 0.f;
+    for (int t = 0; t < p.C; ++t) s += ld_f(Z + (size_t)t * d + j);
+    m[j] = s / (float)p.C;
+  }
+  __syncthreads();
+  const T *S = static_cast<const T *>(p.slots) + (2LL * o + p.sel[o]) * p.slot_elems + p.layer_off;
+  T *D = static_cast<T *>(p.slots) + (2LL * o + 1 - p.sel[o]) * p.slot_elems + p.layer_off;
+  bool bad = false;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (size_t)d * d;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / d), j = (int)(idx - (size_t)i * d);
+    const T st = st_cvt<T>(fmaf(p.eta * m[i], m[j], ld_f(S + idx)));
+    bad |= !isfinite(ld_f(&st));
+    D[idx] = st;
+  }
+  if (bad) atomicOr(p.mfail + o, 1);
+}
+
 }  // namespace
+
+cudaError_t launch_write_rule1(int dtype, const WriteParams &p, cudaStream_t s) {
+  const size_t smem = (size_t)p.d_ff * 4;
+  const int per = (int)std::min<size_t>(((size_t)p.d_ff * p.d_ff + 255) / 256, (size_t)device_sm_count());
+  dim3 grid(std::max(1, per), p.n);
+  if (dtype == 1) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(write_rule1_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    write_rule1_kernel<__nv_bfloat16><<<grid, 256, smem, s>>>(p);
+  } else {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(write_rule1_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    write_rule1_kernel<float><<<grid, 256, smem, s>>>(p);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_write_simt(int dtype, const WriteParams &p, cudaStream_t s) {
   dim3 grid((p.d_ff + TJ - 1) / TJ, (p.d_model + TI - 1) / TI, p.n);

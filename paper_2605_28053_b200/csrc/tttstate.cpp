@@ -113,7 +113,8 @@ static ttt_status check_shape(const ttt_shape *s) {
   const int vec = s->dtype == TTT_BF16 ? 8 : 4;
   if (s->d_ff % vec) return fail(TTT_E_SHAPE, "d_ff must be a multiple of 8 (bf16) / 4 (fp32)");
   if (s->d_model % 4) return fail(TTT_E_SHAPE, "d_model must be a multiple of 4");
-  if (s->rule != 0) return fail(TTT_E_SHAPE, "only rule 0 (chunk outer-product sum) is built on the GPU");
+  if (s->rule != 0 && !(s->rule == 1 && s->backend == TTT_FAST_WEIGHT && s->d_model == s->d_ff))
+    return fail(TTT_E_SHAPE, "rule 1 (SPEC mean rule) needs the fast-weight backend and d_model == d_ff");
   return TTT_OK;
 }
 
@@ -445,7 +446,7 @@ ttt_status read_apply_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec
   }
   // f3: with C = 1 every step is a WRITE whose evidence is this token only, so the
   // candidate is written here, in the same pass over ΔW (write_commit then only commits).
-  const bool fuse = g->effect == TTT_WRITE && sh.chunk == 1 && sh.backend == TTT_FAST_WEIGHT &&
+  const bool fuse = g->effect == TTT_WRITE && sh.chunk == 1 && sh.backend == TTT_FAST_WEIGHT && sh.rule == 0 &&
                     g_write_impl.load() != 1;
   int need_evict = 0;
   if (fuse)
@@ -671,7 +672,8 @@ ttt_status write_commit_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerR
   if (!fused && need_evict > (int)p->free_ckpt.size())
     return fail(TTT_E_POOL_FULL, "no free checkpoint slot for a pinned snapshot");
   const int impl = g_write_impl.load();
-  const bool use_tc = sh.dtype == TTT_BF16 && impl != 1 && write_tc_supported(sh.d_model, sh.d_ff, sh.chunk, sh.n_layers);
+  const bool use_tc = sh.rule == 0 && sh.dtype == TTT_BF16 && impl != 1 &&
+                      write_tc_supported(sh.d_model, sh.d_ff, sh.chunk, sh.n_layers);
   if (!fused && impl == 2 && !use_tc) return fail(TTT_E_SHAPE, "tcgen05 WRITE kernel does not support this shape");
   bool forced = false;
   if (fail_mask)
@@ -740,7 +742,7 @@ ttt_status write_commit_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerR
         wp.layer_off = (long long)l * p->E;
         wp.tz_layer = (long long)l * sh.chunk * sh.d_ff;
         wp.tv_layer = (long long)l * sh.chunk * sh.d_model;
-        cudaError_t e = launch_write_simt(sh.dtype, wp, s);
+        cudaError_t e = sh.rule == 1 ? launch_write_rule1(sh.dtype, wp, s) : launch_write_simt(sh.dtype, wp, s);
         if (e != cudaSuccess) return cuda_fail(e, "write launch");
       }
     }

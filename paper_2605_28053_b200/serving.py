@@ -36,13 +36,13 @@ class Engine:
     def __init__(self, d_model: int, d_ff: int, chunk: int, n_layers: int, dtype: str, max_owners: int,
                  w_down: torch.Tensor, n_ckpt: int = 0, mode: int = capi.MODE_FULL, B: int = 8, w: int = 0,
                  shape_id: int = 0, placement: int = 0, device=None, eta: float = 0.01,
-                 backend: int = capi.FAST_WEIGHT, rank: int = 0):
+                 backend: int = capi.FAST_WEIGHT, rank: int = 0, rule: int = 0):
         device = torch.device(device) if device is not None else w_down.device
         assert w_down.is_cuda, "w_down must be a device tensor"
         self.d_model, self.d_ff, self.chunk, self.n_layers, self.dtype = d_model, d_ff, chunk, n_layers, dtype
         self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float32
         self.eta = float(torch.tensor(eta, dtype=torch.float32))
-        self.shape = capi.make_shape(d_model, d_ff, chunk, n_layers, dtype, backend=backend, rank=rank)
+        self.shape = capi.make_shape(d_model, d_ff, chunk, n_layers, dtype, backend=backend, rank=rank, rule=rule)
         self.backend, self.rank = backend, rank
         self.max_owners = max_owners
         self.arena_bytes = capi.tttstate_pool_bytes(self.shape, max_owners, n_ckpt)

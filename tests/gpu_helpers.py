@@ -79,11 +79,16 @@ class HostGenInputs(InputSource):
 
 
 def make_engine(tr, device="cuda", n_ckpt=4, max_owners=None, mode=None, B=None, w=None):
-    W = to_dev(np.stack([tr.w_down(l) for l in range(tr.n_layers)]), tr.dtype, device)
+    if tr.rule == 1:                       # SPEC-compat rule 1: the base is the identity
+        eye = np.eye(tr.d_model, tr.d_ff)
+        one = (eye * 0x3F80).astype(np.uint16) if tr.dtype == "bf16" else eye.astype(np.float32)
+        W = to_dev(np.stack([one] * tr.n_layers), tr.dtype, device)
+    else:
+        W = to_dev(np.stack([tr.w_down(l) for l in range(tr.n_layers)]), tr.dtype, device)
     return Engine(tr.d_model, tr.d_ff, tr.chunk, tr.n_layers, tr.dtype,
                   max_owners or tr.n_streams + 2, W, n_ckpt=n_ckpt,
                   mode=tr.mode if mode is None else mode, B=tr.B if B is None else B,
-                  w=tr.w if w is None else w, eta=tr.eta, backend=tr.backend, rank=tr.rank)
+                  w=tr.w if w is None else w, eta=tr.eta, backend=tr.backend, rank=tr.rank, rule=tr.rule)
 
 
 def read_lowrank(eng, tr, owner, l):

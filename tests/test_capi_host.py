@@ -175,3 +175,14 @@ def test_serve_step_validates_before_side_effects_on_a_host_pool():
     assert capi.tttstate_last_commit_seq(p) == 0
     capi.ttt_planner_destroy(pl)
     capi.tttstate_pool_destroy(p)
+
+
+def test_rule1_shape_checks():
+    """SPEC-compat rule 1 is accepted for a square fast-weight pool only."""
+    ok = capi.make_shape(16, 16, 4, 1, "fp32", rule=1)
+    p = capi.tttstate_pool_create(ok, 0, 0, 4, 0, None, 0, None)
+    capi.tttstate_pool_destroy(p)
+    for bad in (capi.make_shape(8, 16, 4, 1, "fp32", rule=1), capi.make_shape(16, 16, 4, 1, "fp32", rule=2)):
+        with pytest.raises(capi.TTTError) as e:
+            capi.tttstate_pool_create(bad, 0, 0, 4, 0, None, 0, None)
+        assert e.value.status == 11

@@ -281,3 +281,43 @@ def test_determinism_bitwise_rerun():
     assert runs[0][0] == runs[1][0]
     assert runs[0][1] == runs[1][1]
     assert runs[0][2] == runs[1][2]
+
+
+@pytest.mark.parametrize("dtype,chunk", [("fp32", 4), ("bf16", 8), ("fp32", 1)])
+def test_rule1_spec_mean_rule_parity(dtype, chunk):
+    """SPEC-compat rule 1 on the GPU (S:188 y = x + ΔW x, S:206 / S:215
+    ΔW += η m mᵀ with m the chunk mean): a square trace with snapshots, rollbacks and an injected
+    failure against the oracle's rule-1 arithmetic; the base W_down is the identity."""
+    tr = T.uniform_small(n_streams=4, n_layers=2, d_model=96, d_ff=96, chunk=chunk, n_steps=3 * chunk + 1,
+                         dtype=dtype, rule=1, seed=17,
+                         controls={(1, chunk - 1): ["snapshot"], (1, chunk): ["rollback"], (2, 2 * chunk - 1): ["fail"]})
+    ref, src, log, eng = _run(tr)
+    _compare(tr, ref, src, log, eng)
+
+
+def test_rule1_spec_worked_example_s219():
+    """W = 0 (ΔW_0), z = (1, 1) twice (m = (1, 1)), η = 0.01 -> ΔW = 0.01·[[1,1],[1,1]]
+    (d = 2 is below the kernels' vector width, so d = 8 with the example in the leading 2×2 block
+    and zeros elsewhere); y on the boundary token = x + ΔW_0 x = x."""
+    d, C = 8, 2
+    W = torch.eye(d, device=DEV).unsqueeze(0).contiguous()
+    from paper_2605_28053_b200.serving import Engine
+    eng = Engine(d, d, C, 1, "fp32", 2, W, eta=0.01, rule=1)
+    pool = eng.pool
+    capi.tttstate_alloc(pool, 5)
+    x = torch.zeros(1, d, device=DEV)
+    x[0, :2] = 1.0
+    v = torch.zeros(1, d, device=DEV)
+    Y = torch.empty(1, d, device=DEV)
+    for effect in (capi.READ, capi.WRITE):
+        g = capi.Group(effect, [5])
+        capi.read_apply(pool, g, 0, x, None, v, None, Y)
+        assert torch.equal(Y, x)                    # ΔW_0 = 0: y = x (S:192)
+        if effect == capi.READ:
+            capi.tttstate_step_done(pool, g)
+    assert capi.write_commit(pool, capi.Group(capi.WRITE, [5]), 0.01) == [1]
+    dw = capi.tttstate_read_payload(pool, 5, 0, d, d, "fp32")
+    ref = np.zeros((d, d), dtype=np.float32)
+    ref[:2, :2] = np.float32(0.01)
+    assert np.array_equal(dw, ref) and capi.tttstate_version(pool, 5) == 1
+    eng.close()
