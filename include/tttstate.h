@@ -41,7 +41,7 @@
  *    dropped.  An owner's latest commit is "confirmed" (the mirror corrected
  *    from the device's record, waiting on that commit's event, normally long
  *    complete) by every call that relies on its committed version or slot:
- *    tttstate_version, tttstate_snapshot, rollback, tttstate_fork (source),
+ *    tttstate_version, tttstate_snapshot, tttstate_fork (source),
  *    write_commit / fused read_apply of an owner holding a checkpoint, and
  *    tttstate_sync (all owners).  READ launches use the device slot table, so
  *    they always see the device's committed state.

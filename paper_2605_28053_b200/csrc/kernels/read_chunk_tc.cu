@@ -473,8 +473,8 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
   if (LR && p.trace && threadIdx.x == 0) {
     stamp(7);
-    printf("LRT %d %llu %llu %llu %llu %llu %llu %llu %llu\n", (int)blockIdx.x, ts[0], ts[1], ts[2], ts[3], ts[4],
-           ts[5], ts[6], ts[7]);
+    printf("LRT %d %llu %llu %llu %llu %llu %llu %llu %llu %d\n", (int)blockIdx.x, ts[0], ts[1], ts[2], ts[3], ts[4],
+           ts[5], ts[6], ts[7], p.layer);
   }
   if (LR && threadIdx.x == 0) {                    // the last CTA out re-arms the counters
     __threadfence();

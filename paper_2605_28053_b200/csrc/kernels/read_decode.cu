@@ -727,11 +727,15 @@ cudaError_t launch_mma(const ReadParams &p, cudaStream_t s) {
   const size_t smem = (size_t)kMaxReadMembers * mma_nvp(p.d_ff / 8) * 16;
   static size_t configured = 0;
   if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(read_decode_mma_kernel<FUSE, L2H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(read_decode_mma_kernel<FUSE, L2H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 * 1024));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(read_decode_mma_kernel<FUSE, L2H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)std::max<size_t>(smem, 48 * 1024));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
+  static const bool pre1 = !getenv("TTT_READ_PRE1") || atoi(getenv("TTT_READ_PRE1")) != 0;
   static const bool pdl = !getenv("TTT_PDL") || atoi(getenv("TTT_PDL")) != 0;
   static const int order = getenv("TTT_READ_ORDER") ? atoi(getenv("TTT_READ_ORDER")) : 1;
   static const int dyn = getenv("TTT_READ_DYN") ? atoi(getenv("TTT_READ_DYN")) : 1;
@@ -750,7 +754,8 @@ cudaError_t launch_mma(const ReadParams &p, cudaStream_t s) {
   q.order = order;
   q.dyn = order == 1 ? dyn : 0;
   q.xtma = xtma;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, read_decode_mma_kernel<FUSE, L2H>, q);
+  cudaError_t e = pre1 ? cudaLaunchKernelEx(&cfg, read_decode_mma_kernel<FUSE, L2H, true>, q)
+                       : cudaLaunchKernelEx(&cfg, read_decode_mma_kernel<FUSE, L2H, false>, q);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }

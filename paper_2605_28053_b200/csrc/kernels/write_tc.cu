@@ -65,6 +65,7 @@ struct TcParams {
   int *mfail;
   int *arrive;                                    // fused commit: CTA arrival counter (self-resetting)
   int fuse_commit;
+  int early_dep;                                  // trigger the dependent launch at entry (PDL)
   int owner_idx[kMaxGroup];
   CommitParams cp;
 };
@@ -182,8 +183,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // PDL: only the prologue above overlaps the previous kernel (the step's last READ);
-  // the tails, slots and the active-slot table are read after the wait.
-  asm volatile("griddepcontrol.launch_dependents;");
+  // the tails, slots and the active-slot table are read after the wait.  The dependent launch
+  // is NOT triggered at entry (TTT_WRITE_EARLY_DEP=1 restores it): with this persistent grid
+  // the next step's READ CTAs, launched early, took SMs as WRITE CTAs retired and bursty WRITE
+  // steps (config 3: a 1-member WRITE in every other step) ran 8.42 instead of 7.10 ms per
+  // step; the kernel durations themselves were unchanged (ncu), config 2 is unaffected.
+  if (p.early_dep) asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
@@ -420,9 +425,10 @@ cudaError_t launch_cfg(const Maps &m, const TcParams &p, int tiles, size_t smem,
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
+  static const bool pdl = !getenv("TTT_WRITE_PDL") || atoi(getenv("TTT_WRITE_PDL")) != 0;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, write_tc_kernel<BN, SB, ST, HINT>, m.V, m.Z, m.W, p);
@@ -456,6 +462,8 @@ cudaError_t launch_write_tc(const WriteParams &wp, const CommitParams *cp, int *
   p.mfail = wp.mfail;
   p.arrive = arrive;
   p.fuse_commit = cp != nullptr;
+  static const int early_dep = getenv("TTT_WRITE_EARLY_DEP") ? atoi(getenv("TTT_WRITE_EARLY_DEP")) : 0;
+  p.early_dep = early_dep;
   for (int b = 0; b < wp.n; ++b) p.owner_idx[b] = wp.owner_idx[b];
   if (cp) p.cp = *cp;
   const int tiles = wp.n * (wp.d_model / BM) * (wp.d_ff / k.BN);   // per layer (grid = min(SMs, tiles))

@@ -734,9 +734,10 @@ ttt_status write_commit_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerR
     wp.max_owners = p->max_owners; wp.max_slots = 2 * p->max_owners + p->n_ckpt;
     for (int b = 0; b < g->n; ++b) wp.owner_idx[b] = recs[b]->idx;
     if (use_tc) {                                   // every layer in one launch, commit fused
-      cudaError_t e = launch_write_tc(wp, &cp, p->d_wctr(), s);
+      static const bool fuse_commit = !getenv("TTT_WRITE_FUSE_COMMIT") || atoi(getenv("TTT_WRITE_FUSE_COMMIT")) != 0;
+      cudaError_t e = launch_write_tc(wp, fuse_commit ? &cp : nullptr, p->d_wctr(), s);
       if (e != cudaSuccess) return cuda_fail(e, "write launch");
-      committed = true;
+      committed = fuse_commit;
     } else {
       for (int l = 0; l < sh.n_layers; ++l) {
         wp.layer_off = (long long)l * p->E;
@@ -817,7 +818,11 @@ ttt_status rollback(ttt_pool *p, uint64_t owner, uint64_t *v_out, void *stream) 
   if (st != TTT_OK) return st;
   if (!r->has_ckpt) return fail(TTT_E_NO_CHECKPOINT, "owner " + std::to_string(owner));
   if (p->host_only) return fail(TTT_E_NO_DEVICE, "host-only pool");
-  if ((st = confirm(p, *r)) != TTT_OK) return st;
+  // No confirmation needed (and no host wait right after a speculative WRITE): the restored
+  // (slot, version) come from the checkpoint, and a copy back from the checkpoint pool may land
+  // in either slot of the pair; the pending commit's outcome is superseded by the rollback
+  // (its refusal record, if any, is still logged for tttstate_refusals).
+  r->pending_seq = 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int new_sel;
   if (r->ckpt_pool < 0) {

@@ -21,6 +21,7 @@ outcome.  PyTorch provides the device arena and streams only.
 """
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -134,7 +135,8 @@ class Server:
     def __init__(self, eng: Engine, tr, src: InputSource, stream=None, profile: bool = False,
                  profile_every: int = 1, native: bool = True):
         self.eng, self.tr, self.src, self.stream = eng, tr, src, stream
-        self.profile, self.profile_every, self.native = profile, max(1, profile_every), native
+        self.profile, self.profile_every = profile, max(1, profile_every)
+        self.native = native and os.environ.get("TTT_NATIVE_STEP", "1") != "0"   # A/B switch: per-operator calls
         self.log = RunLog()
         self.owners = [tr.owner(s) for s in range(tr.n_streams)]
         self.by_owner = {o: s for s, o in enumerate(self.owners)}
@@ -186,10 +188,9 @@ class Server:
         for op in tr.controls_at(s, self.pos[s]):
             if op == "snapshot":
                 capi.tttstate_snapshot(pool, o, stream)
-            elif op == "rollback":
-                vb = capi.tttstate_version(pool, o)
+            elif op == "rollback":                              # v_before comes from drain()'s replay
                 va = capi.rollback(pool, o, stream)
-                self._items.append(("rb", s, self.pos[s], vb, va))
+                self._items.append(("rb", s, self.pos[s], None, va))
                 log.rollbacks += 1
             elif op == "fork":                                  # new lineage
                 k = self.forks.get(s, 0)
@@ -363,7 +364,7 @@ class Server:
                 one(it[1], it[2], False)
             else:                                               # ("rb", s, p, v_before, v_after)
                 _, s, p, vb, va = it
-                log.commits.append((s, p, vb, va, "rolled_back"))
+                log.commits.append((s, p, vt[s] if vb is None else vb, va, "rolled_back"))
                 vt[s] = va
         self._items = []
 

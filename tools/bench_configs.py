@@ -161,11 +161,15 @@ def run(name: str, windows: int, warmup: int):
     fb0, df0 = srv.log.fallbacks, srv.log.device_failures
     rb0 = srv.log.rollbacks
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import time
+    t0 = time.perf_counter()
     e0.record(stream)
     for _ in range(windows * tr.chunk):
         srv.step()
     e1.record(stream)
+    t_enq = time.perf_counter() - t0
     torch.cuda.synchronize(dev)
+    t_wall = time.perf_counter() - t0
     ms = e0.elapsed_time(e1)
     srv.drain()                                    # confirm the window's commits (device refusals)
     tokens = sum(srv.log.census.values()) - sum(census0.values())
@@ -174,7 +178,9 @@ def run(name: str, windows: int, warmup: int):
            "census": {"READ": srv.log.census[0] - census0.get(0, 0), "WRITE": srv.log.census[1] - census0.get(1, 0)},
            "fallbacks": srv.log.fallbacks - fb0, "device_failures": srv.log.device_failures - df0,
            "rollbacks": srv.log.rollbacks - rb0,
-           "roofline_tok_s": ROOFLINE.get(name)}
+           "roofline_tok_s": ROOFLINE.get(name),
+           "host_enqueue_ms_per_step": 1e3 * t_enq / (windows * tr.chunk), "device_ms_per_step": ms / (windows * tr.chunk),
+           "host_wall_over_device": 1e3 * t_wall / ms}
     out["frac_of_roofline"] = out["tok_s"] / out["roofline_tok_s"] if out["roofline_tok_s"] else None
     out["parity"] = sampled_parity(srv, eng, tr, src, W)
     assert out["parity"]["ok"], out["parity"]

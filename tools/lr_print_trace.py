@@ -43,6 +43,10 @@ torch.cuda.synchronize()
 '''
 
 
+def n_ctas(rows):
+    return max(r[0] for r in rows) + 1
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rank", type=int, default=16)
@@ -52,11 +56,12 @@ def main():
     out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, a.members, a.rank)], env=env, capture_output=True,
                          text=True, check=True).stdout
     rows = [list(map(int, ln.split()[1:])) for ln in out.splitlines() if ln.startswith("LRT ")]
-    # group into launches by entry time (launches are serial)
+    # group into launches: launches run in order and alternate layers; a launch's CTAs all enter
+    # before the next launch's (1 CTA per SM, the next grid waits for SMs to free up)
     rows.sort(key=lambda r: r[1])
     launches, cur = [], []
     for r in rows:
-        if cur and r[1] - max(x[8] for x in cur) > 0:       # entered after every CTA of cur exited
+        if cur and (r[9] != cur[0][9] or len(cur) == n_ctas(rows)):
             launches.append(cur)
             cur = []
         cur.append(r)
