@@ -72,6 +72,7 @@ struct ChunkParams {
   int x_rowmap;                  // X map is [rows][d_ff]: row block b starts at row 128·b
   int cooperative;               // LR: launch cooperatively (co-residency guaranteed)
   int trace;                     // LR: TTT_LR_PRINT=1 prints per-CTA %globaltimer phase stamps (profiling)
+  int early_dep;                 // PDL: trigger the dependent launch at entry (TTT_CHUNK_EARLY_DEP)
   int owner_idx[kMaxGroup];
   LrFused lr;
 };
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   // PDL: the prologue above (barriers, TMEM, tensor-map prefetch) overlaps the previous
   // kernel's tail; everything below may depend on it (X, slots, sel, workspace, counters).
-  asm volatile("griddepcontrol.launch_dependents;");
+  if (p.early_dep) asm volatile("griddepcontrol.launch_dependents;");
   // low-rank launch: W_down is never written by any kernel, so the first tile's first W boxes
   // are requested before the wait and stream while the previous kernel drains (X, the slot
   // table and the rest after it): -1 % per layer at R = 16 / 64; the chunk READ measured
@@ -621,6 +622,8 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
   p.cooperative = cl.cooperative;
   static const int lr_print = getenv("TTT_LR_PRINT") ? atoi(getenv("TTT_LR_PRINT")) : 0;
   p.trace = lr_print;
+  static const int early_dep = getenv("TTT_CHUNK_EARLY_DEP") ? atoi(getenv("TTT_CHUNK_EARLY_DEP")) : 1;
+  p.early_dep = early_dep;
   for (int b = 0; b < cl.n; ++b) p.owner_idx[b] = cl.owner_idx[b];
   const int sms = device_sm_count();
   const NPlan np = plan_n(cl.d_model, cl.n * std::max(1, cl.ksplit), sms);
