@@ -105,7 +105,18 @@ struct ChunkLaunch {
   int *lr_ctr = nullptr;                    // fused mode counters [u_done, exit, tickets...], zero at rest
   int x_rowmap = 0;                         // X is [rows][d_ff] (2-D map, rows past n zero-filled)
   int cooperative = 0;                      // fused mode: cooperative launch (several low-rank pools live)
+  const int *d_members = nullptr;           // device member table [5][kMaxGroup]: owner_idx, x_row, v_row,
+                                            // y_row, tail_pos (kernel params stay small: see MemberTable)
 };
+
+// Per-member arrays of a chunk / low-rank READ group, kept in the pool's device workspace
+// instead of the kernel parameters: a ~7 KB parameter block cost ~14 µs of host time per launch
+// (measured r2), while the table changes at most once per decode step (every layer of a step
+// sees the same rows and tail positions), so it is uploaded by one small kernel when it changes.
+struct MemberTable {
+  int a[5][kMaxGroup];           // owner_idx, x_row, v_row, y_row, tail_pos
+};
+cudaError_t launch_member_upload(const MemberTable &t, int n, int *dst, cudaStream_t s);
 
 // NEXT f1: low-rank delta READ / WRITE (DeltaAdapterState).
 struct LowRankRead {

@@ -52,6 +52,13 @@ __global__ void copy_tail_bytes(unsigned char *dst, const unsigned char *src, si
   for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
+__global__ void member_upload_kernel(const __grid_constant__ MemberTable t, int n, int *dst) {
+  for (int i = threadIdx.x; i < 5 * n; i += blockDim.x) {
+    const int k = i / n, b = i - k * n;
+    dst[k * kMaxGroup + b] = t.a[k][b];
+  }
+}
+
 __global__ void set_state_kernel(int *sel, unsigned long long *version, int *mfail, int idx, int s,
                                  unsigned long long v) {
   sel[idx] = s;
@@ -79,6 +86,12 @@ cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s
                                      static_cast<const unsigned char *>(src) + n16 * 16, bytes % 16);
     count_launch();
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_member_upload(const MemberTable &t, int n, int *dst, cudaStream_t s) {
+  member_upload_kernel<<<1, 256, 0, s>>>(t, n, dst);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -55,7 +55,7 @@ struct LrFused {
   float *u;                      // [n][R]
   float *bu;                     // [n][d_model] Bᵀu per member (fp32)
   int *ctr;                      // [0] members whose Bᵀu is done, [1] CTAs exited, [2..] slab tickets per (row block, N block)
-  int x_row[kMaxGroup], v_row[kMaxGroup], y_row[kMaxGroup], tail_pos[kMaxGroup];
+  const int *x_row, *v_row, *y_row, *tail_pos;   // device member table (MemberTable rows 1-4)
 };
 
 struct ChunkParams {
@@ -73,7 +73,7 @@ struct ChunkParams {
   int cooperative;               // LR: launch cooperatively (co-residency guaranteed)
   int trace;                     // LR: TTT_LR_PRINT=1 prints per-CTA %globaltimer phase stamps (profiling)
   int early_dep;                 // PDL: trigger the dependent launch at entry (TTT_CHUNK_EARLY_DEP)
-  int owner_idx[kMaxGroup];
+  const int *owner_idx;          // device member table row 0
   LrFused lr;
 };
 
@@ -624,7 +624,8 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
   p.trace = lr_print;
   static const int early_dep = getenv("TTT_CHUNK_EARLY_DEP") ? atoi(getenv("TTT_CHUNK_EARLY_DEP")) : 1;
   p.early_dep = early_dep;
-  for (int b = 0; b < cl.n; ++b) p.owner_idx[b] = cl.owner_idx[b];
+  if (!cl.d_members) return cudaErrorInvalidValue;
+  p.owner_idx = cl.d_members;
   const int sms = device_sm_count();
   const NPlan np = plan_n(cl.d_model, cl.n * std::max(1, cl.ksplit), sms);
   if (np.T == 0) return cudaErrorInvalidValue;
@@ -646,13 +647,10 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
     p.lr.u = q.u;
     p.lr.bu = q.Y32 + (size_t)kMaxKSplit * q.y32_slab;
     p.lr.ctr = cl.lr_ctr;
-    for (int b = 0; b < q.n; ++b) {
-      p.owner_idx[b] = q.owner_idx[b];
-      p.lr.x_row[b] = q.x_row[b];
-      p.lr.v_row[b] = q.v_row[b];
-      p.lr.y_row[b] = q.y_row[b];
-      p.lr.tail_pos[b] = q.tail_pos[b];
-    }
+    p.lr.x_row = cl.d_members + kMaxGroup;
+    p.lr.v_row = cl.d_members + 2 * kMaxGroup;
+    p.lr.y_row = cl.d_members + 3 * kMaxGroup;
+    p.lr.tail_pos = cl.d_members + 4 * kMaxGroup;
     p.Vt = q.Vt;
     p.tailZ = q.tailZ;
     p.tailV = q.tailV;

@@ -32,6 +32,7 @@ struct OwnerRec {
 
 struct Layout {
   size_t slots = 0, tailZ = 0, tailV = 0, sel = 0, ver = 0, flags = 0, mfail = 0, rlog = 0, P = 0, tickets = 0;
+  size_t members = 0;                              // MemberTable (chunk / low-rank READ groups)
   size_t Xg = 0, Y32 = 0, U = 0, Ctr = 0, total = 0;   // low-rank READ workspace
 };
 
@@ -65,6 +66,8 @@ struct ttt_pool {
   std::vector<cudaEvent_t> ev_ring;                 // event recorded after commit seq k: ev_ring[k % size]
   ttt::HostOwnerState *hstate = nullptr;            // [max_owners], cudaHostAllocMapped (host view)
   ttt::HostOwnerState *hstate_dev = nullptr;        // the same memory as the kernels address it
+  ttt::MemberTable m_last{};                        // member table last uploaded to lay.members
+  int m_n = -1;
 
   // device pointers (valid when !host_only)
   unsigned char *slot_ptr(long long slot) const {
@@ -76,6 +79,7 @@ struct ttt_pool {
   int *d_fail_count() const { return reinterpret_cast<int *>(arena + lay.flags); }
   int *d_rlog_count() const { return reinterpret_cast<int *>(arena + lay.flags + 16); }
   int *d_mfail() const { return reinterpret_cast<int *>(arena + lay.mfail); }
+  int *d_members() const { return reinterpret_cast<int *>(arena + lay.members); }
   int *d_wctr() const { return reinterpret_cast<int *>(arena + lay.flags + 32); }   // fused-commit arrivals
   ttt::RefusalRec *d_rlog() const { return reinterpret_cast<ttt::RefusalRec *>(arena + lay.rlog); }
 };

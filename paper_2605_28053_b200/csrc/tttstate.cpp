@@ -86,6 +86,7 @@ Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt) {
   L.flags = off;   off = align_up(off + 64, 256);                  // fail_count, refusal-log counter
   L.mfail = off;   off = align_up(off + (size_t)max_owners * 4, 256);  // per-owner device-failure flags
   L.rlog = off;    off = align_up(off + (size_t)kRefusalLog * sizeof(RefusalRec), 256);
+  L.members = off; off = align_up(off + sizeof(MemberTable), 256);
   // READ partials: base K-chunk slabs [kc][8][d_model] (kc ≤ ⌈d_ff/512⌉) + ΔW [8][d_model]
   L.P = off;       off = align_up(off + ((size_t)(s.d_ff + 511) / 512 + 1) * kMaxReadMembers * s.d_model * 4, 256);
   L.tickets = off; off = align_up(off + (size_t)s.d_model * 4, 1024);
@@ -186,6 +187,19 @@ ttt_status confirm(ttt_pool *p, OwnerRec &r) {
   r.sel = h->sel;
   r.pending_seq = 0;
   return TTT_OK;
+}
+
+// Upload a chunk / low-rank READ group's member table unless the device copy already holds it
+// (every layer of a decode step reuses the same rows and tail positions: one upload per step).
+cudaError_t upload_members(ttt_pool *p, const MemberTable &t, int n, cudaStream_t s) {
+  bool same = p->m_n == n;
+  for (int k = 0; k < 5 && same; ++k) same = std::memcmp(t.a[k], p->m_last.a[k], (size_t)n * sizeof(int)) == 0;
+  if (same) return cudaSuccess;
+  cudaError_t e = launch_member_upload(t, n, p->d_members(), s);
+  if (e != cudaSuccess) return e;
+  for (int k = 0; k < 5; ++k) std::memcpy(p->m_last.a[k], t.a[k], (size_t)n * sizeof(int));
+  p->m_n = n;
+  return cudaSuccess;
 }
 
 cudaError_t evict_pinned(ttt_pool *p, OwnerRec &r, cudaStream_t s) {
@@ -484,7 +498,19 @@ ttt_status read_apply_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec
       lp.y_row[b] = y_rows ? y_rows[b] : b;
       lp.tail_pos[b] = recs[b]->tail_len;
     }
+    {
+      MemberTable mt;
+      for (int b = 0; b < g->n; ++b) {
+        mt.a[0][b] = lp.owner_idx[b];
+        mt.a[1][b] = lp.x_row[b];
+        mt.a[2][b] = lp.v_row[b];
+        mt.a[3][b] = lp.y_row[b];
+        mt.a[4][b] = lp.tail_pos[b];
+      }
+      CUDA_TRY(upload_members(p, mt, g->n, s));
+    }
     ChunkLaunch cl{};
+    cl.d_members = p->d_members();
     cl.n = (g->n + 127) / 128; cl.d_model = sh.d_model; cl.d_ff = sh.d_ff; cl.C = 128; cl.L = sh.n_layers;
     cl.layer = layer; cl.max_slots = 1; cl.sel = p->d_sel();
     cl.X = lp.Xg; cl.w_down = p->w_down; cl.slots = p->w_down;
@@ -632,6 +658,13 @@ ttt_status read_apply_chunk(ttt_pool *p, const ttt_group *g, int32_t layer, cons
   cl.tz_layer = (long long)layer * sh.chunk * sh.d_ff;
   cl.tv_layer = (long long)layer * sh.chunk * sh.d_model;
   for (int b = 0; b < g->n; ++b) cl.owner_idx[b] = recs[b]->idx;
+  {
+    MemberTable mt;
+    std::memset(&mt, 0, sizeof(mt));
+    for (int b = 0; b < g->n; ++b) mt.a[0][b] = recs[b]->idx;
+    CUDA_TRY(upload_members(p, mt, g->n, static_cast<cudaStream_t>(stream)));
+  }
+  cl.d_members = p->d_members();
   cudaError_t e = launch_read_chunk(cl, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "read_chunk launch");
   for (int b = 0; b < g->n; ++b) {
