@@ -241,7 +241,7 @@ def _window_class():
         def step_io(self, ss, ps):               # the native step: one row map for every layer
             C, S, tr = self.tr.chunk, self.S, self.tr
             rows = [(p % C) * S + s for s, p in zip(ss, ps)]
-            return StepIO(self.X, C * S * tr.d_ff, self.V, C * S * tr.d_model, self.Y, C * S * tr.d_model, rows)
+            return StepIO(self.X, C * S * tr.d_ff, self.V, C * S * tr.d_model, self.Y, C * S * tr.d_model, rows, C * S)
 
     return HBMWindow
 

@@ -275,6 +275,8 @@ typedef struct {
   const int32_t *rows;
   void *ev_write_begin, *ev_write_end;   /* profiling (may be NULL): cudaEvent_t recorded right before the
                                           * step's first WRITE group's WRITE launches and after its commit */
+  int64_t rows_total;                    /* rows of each layer's X / Vt / Y (0: unknown).  Lets a low-rank
+                                          * group with contiguous rows skip the gather of its X rows */
 } ttt_step_io;
 
 /* Host buffers the step fills (caller-owned).  groups/owner_buf as plan_batch;

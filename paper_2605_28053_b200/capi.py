@@ -55,7 +55,8 @@ class ttt_group(C.Structure):
 class ttt_step_io(C.Structure):
     _fields_ = [("X", C.c_void_p), ("x_layer_stride", C.c_int64), ("Vt", C.c_void_p), ("v_layer_stride", C.c_int64),
                 ("Y", C.c_void_p), ("y_layer_stride", C.c_int64), ("resid", C.c_void_p), ("r_layer_stride", C.c_int64),
-                ("rows", C.POINTER(C.c_int32)), ("ev_write_begin", C.c_void_p), ("ev_write_end", C.c_void_p)]
+                ("rows", C.POINTER(C.c_int32)), ("ev_write_begin", C.c_void_p), ("ev_write_end", C.c_void_p),
+                ("rows_total", C.c_int64)]
 
 
 class ttt_step_out(C.Structure):
@@ -456,7 +457,7 @@ class StepBuffers:
 
 def tttstate_serve_step(pool, pl, bufs: StepBuffers, n: int, clock: int, X, x_stride, Vt, v_stride, Y, y_stride,
                         eta: float, n_fail: int = 0, resid=None, r_stride: int = 0, stream=None,
-                        ev_write=(None, None)):
+                        ev_write=(None, None), rows_total: int = 0):
     """One Alg. 1 iteration for bufs.owners[:n] at rows bufs.rows[:n] (fill those arrays first)."""
     if pool in _POOL_INFO:
         sh = _POOL_INFO[pool]
@@ -472,6 +473,7 @@ def tttstate_serve_step(pool, pl, bufs: StepBuffers, n: int, clock: int, X, x_st
     io.Y, io.y_layer_stride, io.resid, io.r_layer_stride = _ptr(Y), y_stride, _ptr(resid), r_stride
     io.ev_write_begin = None if ev_write[0] is None else ev_write[0].cuda_event
     io.ev_write_end = None if ev_write[1] is None else ev_write[1].cuda_event
+    io.rows_total = rows_total
     _check(_lib.tttstate_serve_step(pool, pl, bufs.owners, n, clock, C.byref(io), C.c_float(eta),
                                     bufs.fail if n_fail else None, n_fail, C.byref(bufs.out), _stream(stream)))
     return bufs.out

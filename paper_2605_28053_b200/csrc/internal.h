@@ -104,14 +104,16 @@ struct ChunkLaunch {
   const struct LowRankRead *lr = nullptr;   // non-null: fused low-rank READ (u = A x, finish) in this launch
   int *lr_ctr = nullptr;                    // fused mode counters [u_done, exit, tickets...], zero at rest
   int x_rowmap = 0;                         // X is [rows][d_ff] (2-D map, rows past n zero-filled)
+  int x_row0 = 0;                           // x_rowmap: the group's first row in X (TMA row coordinate offset)
+  long long x_rows_total = 0;               // x_rowmap: rows of the X buffer (0: the group's rows only)
   int cooperative = 0;                      // fused mode: cooperative launch (several low-rank pools live)
   const int *d_members = nullptr;           // device member table [5][kMaxGroup]: owner_idx, x_row, v_row,
                                             // y_row, tail_pos (kernel params stay small: see MemberTable)
 };
 
 // Per-member arrays of a chunk / low-rank READ group, kept in the pool's device workspace
-// instead of the kernel parameters: a ~7 KB parameter block cost ~14 µs of host time per launch
-// (measured r2), while the table changes at most once per decode step (every layer of a step
+// instead of the kernel parameters (parameter block ~7 KB -> ~0.6 KB; host per low-rank launch
+// 18.0 -> 16.5 µs, r2): the table changes at most once per decode step (every layer of a step
 // sees the same rows and tail positions), so it is uploaded by one small kernel when it changes.
 struct MemberTable {
   int a[5][kMaxGroup];           // owner_idx, x_row, v_row, y_row, tail_pos
@@ -121,6 +123,8 @@ cudaError_t launch_member_upload(const MemberTable &t, int n, int *dst, cudaStre
 // NEXT f1: low-rank delta READ / WRITE (DeltaAdapterState).
 struct LowRankRead {
   int n, d_model, d_ff, rank;
+  int x_row0 = -1;               // >= 0: the members' X rows are x_row0 .. x_row0 + n - 1 of a buffer
+  long long x_rows_total = 0;    //   with x_rows_total rows (no gather: the GEMM's TMA map offsets them)
   const void *X, *Vt, *resid;
   void *Y, *Xg;
   float *Y32, *u;                // [ksplit][rows][d_model] base product slabs, [n·R][nseg] A·x partials

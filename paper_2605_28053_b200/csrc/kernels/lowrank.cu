@@ -275,7 +275,12 @@ cudaError_t launch_lowrank_read(const LowRankRead &p0, const ChunkLaunch &base0,
   }
   if (mode != 0 && read_chunk_fused_fits(base.n, p.d_model, base.ksplit)) {
     // one launch: base GEMM on tcgen05 + u = A x warps + tail append + finish (read_chunk_tc.cu)
-    if (identity) {
+    if (p.x_row0 >= 0 && p.x_rows_total > 0) {     // contiguous rows of a known buffer: no gather
+      base.X = p.X;
+      base.x_rowmap = 1;
+      base.x_row0 = p.x_row0;
+      base.x_rows_total = p.x_rows_total;
+    } else if (identity) {
       base.X = p.X;
       base.x_rowmap = 1;
     } else {

@@ -69,7 +69,8 @@ struct ChunkParams {
   int nt, w_hi, h;               // N blocks per member; blocks j < h are w_hi wide, the rest w_hi - 16
   float *Y32;
   long long y32_slab;
-  int x_rowmap;                  // X map is [rows][d_ff]: row block b starts at row 128·b
+  int x_rowmap;                  // X map is [rows][d_ff]: row block b starts at row x_row0 + 128·b
+  int x_row0;
   int cooperative;               // LR: launch cooperatively (co-residency guaranteed)
   int trace;                     // LR: TTT_LR_PRINT=1 prints per-CTA %globaltimer phase stamps (profiling)
   int early_dep;                 // PDL: trigger the dependent launch at entry (TTT_CHUNK_EARLY_DEP)
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
           unsigned char *st = smem + s * STAGE;
           const bool pre = it < npre;                       // W box (and the expect) already issued
           if (!pre) mbar_expect_tx(full + s, A_BYTES + (p.delta ? 2 : 1) * b_box);
-          if (p.x_rowmap) tma_load_3d(st, &tmX, full + s, kb * BK, b * BM, 0);
+          if (p.x_rowmap) tma_load_3d(st, &tmX, full + s, kb * BK, p.x_row0 + b * BM, 0);
           else tma_load_3d(st, &tmX, full + s, kb * BK, 0, b);
           if (!pre) tma_load_3d(st + A_BYTES, &tmW, full + s, kb * BK, n0_of(j), p.layer);
           if (p.delta) tma_load_3d(st + A_BYTES + B_BYTES, &tmD, full + s, kb * BK, n0_of(j), slot_l);
@@ -619,6 +620,7 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
   p.ksplit = cl.ksplit < 1 ? 1 : cl.ksplit;
   p.y32_slab = cl.y32_slab;
   p.x_rowmap = cl.x_rowmap;
+  p.x_row0 = cl.x_row0;
   p.cooperative = cl.cooperative;
   static const int lr_print = getenv("TTT_LR_PRINT") ? atoi(getenv("TTT_LR_PRINT")) : 0;
   p.trace = lr_print;
@@ -660,7 +662,9 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
     p.tv_layer = q.tv_layer;
   }
   CUtensorMap mX, mW, mD;
-  const bool xmap_ok = cl.x_rowmap ? cached_map(&mX, cl.X, cl.d_ff, (uint64_t)cl.valid_rows, 1, BK, BM)
+  const bool xmap_ok = cl.x_rowmap ? cached_map(&mX, cl.X, cl.d_ff,
+                                                (uint64_t)(cl.x_rows_total > 0 ? cl.x_rows_total : cl.valid_rows), 1,
+                                                BK, BM)
                                    : cached_map(&mX, cl.X, cl.d_ff, cl.C, cl.n, BK, BM);
   if (!xmap_ok || !cached_map(&mW, cl.w_down, cl.d_ff, cl.d_model, cl.L, BK, np.w_hi) ||
       !cached_map(&mD, cl.delta ? cl.slots : cl.w_down, cl.d_ff, cl.d_model,

@@ -444,7 +444,7 @@ namespace {
 // read_apply after check_group (serve_step resolves the group once for all layers)
 ttt_status read_apply_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec *> &recs, int32_t layer,
                            const void *X, const int32_t *x_rows, const void *Vt, const int32_t *v_rows, void *Y,
-                           const int32_t *y_rows, const void *resid, cudaStream_t s) {
+                           const int32_t *y_rows, const void *resid, cudaStream_t s, long long x_rows_total = 0) {
   ttt_status st;
   const ttt_shape &sh = p->sh;
   if (layer < 0 || layer >= sh.n_layers) return fail(TTT_E_SHAPE, "layer out of range");
@@ -497,6 +497,14 @@ ttt_status read_apply_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec
       lp.v_row[b] = v_rows ? v_rows[b] : b;
       lp.y_row[b] = y_rows ? y_rows[b] : b;
       lp.tail_pos[b] = recs[b]->tail_len;
+    }
+    if (x_rows_total > 0) {                         // serve_step knows the X buffer: contiguous rows need no gather
+      bool contiguous = true;
+      for (int b = 0; b < g->n; ++b) contiguous &= lp.x_row[b] == lp.x_row[0] + b;
+      if (contiguous && lp.x_row[0] >= 0 && lp.x_row[0] + g->n <= x_rows_total) {
+        lp.x_row0 = lp.x_row[0];
+        lp.x_rows_total = x_rows_total;
+      }
     }
     {
       MemberTable mt;
@@ -1004,7 +1012,8 @@ ttt_status tttstate_serve_step(ttt_pool *p, ttt_planner *pl, const uint64_t *own
       unsigned char *Y = static_cast<unsigned char *>(io->Y) + (size_t)l * io->y_layer_stride * es;
       const unsigned char *R = io->resid ? static_cast<const unsigned char *>(io->resid) + (size_t)l * io->r_layer_stride * es
                                          : nullptr;
-      if ((st = read_apply_recs(p, &g, recs, l, X, rows.data(), V, rows.data(), Y, rows.data(), R, s)) != TTT_OK)
+      if ((st = read_apply_recs(p, &g, recs, l, X, rows.data(), V, rows.data(), Y, rows.data(), R, s, io->rows_total)) !=
+          TTT_OK)
         return st;
     }
     if (g.effect == TTT_READ) {                    // UpdateKVAndTailMetadata

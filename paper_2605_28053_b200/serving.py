@@ -96,6 +96,7 @@ class StepIO:
     Y: torch.Tensor
     y_stride: int
     rows: list
+    rows_total: int = 0           # rows of each layer's X / Vt / Y (0: unknown)
 
 
 class InputSource:
@@ -232,7 +233,7 @@ class Server:
         self.plan_s += time.perf_counter() - t0
         out = capi.tttstate_serve_step(eng.pool, eng.planner, bufs, len(active), clock, io.X, io.x_stride, io.Vt,
                                        io.v_stride, io.Y, io.y_stride, tr.eta, n_fail, stream=self.stream,
-                                       ev_write=self._wev)
+                                       ev_write=self._wev, rows_total=io.rows_total)
         t1 = time.perf_counter()
         for s in active:
             self.pending.add(s)

@@ -69,3 +69,33 @@ def test_two_lowrank_pools_on_two_streams():
         assert log.versions == ref.versions and log.commits == ref.commits
         worst = max(nm.normwise_rel_err(src.out[k], ref.outputs[k]) for k in ref.outputs)
         assert worst <= nm.TOL["bf16"], worst
+
+
+def test_lowrank_contiguous_rows_of_a_larger_buffer_no_gather():
+    """The native step tells the library how many rows each layer's X holds (ttt_step_io.rows_total);
+    a low-rank group whose tokens sit in contiguous rows x_row0 .. x_row0 + n - 1 of that buffer runs
+    the fused READ with the TMA row offset instead of gathering X (r2).  Rows start at 37 here."""
+    from paper_2605_28053_b200.serving import StepIO
+
+    class OffsetRows(HostGenInputs):
+        def step_io(self, ss, ps):
+            io = super().step_io(ss, ps)
+            n, off, L = len(ss), 37, len(self.layers)
+            X = torch.zeros(L, n + 80, self.tr.d_ff, dtype=io.X.dtype, device=DEV)
+            V = torch.zeros(L, n + 80, self.tr.d_model, dtype=io.X.dtype, device=DEV)
+            Y = torch.zeros(L, n + 80, self.tr.d_model, dtype=io.X.dtype, device=DEV)
+            X[:, off:off + n] = io.X
+            V[:, off:off + n] = io.Vt
+            return StepIO(X, (n + 80) * self.tr.d_ff, V, (n + 80) * self.tr.d_model, Y, (n + 80) * self.tr.d_model,
+                          [off + i for i in range(n)], n + 80)
+
+    tr = T.config4_lowrank(n_steps=18, n_layers=2, rank=16, d_model=256, d_ff=384, chunk=8, n_streams=24, seed=9)
+    tr = tr.replace(B=24)
+    ref = run_batched(tr)
+    eng = make_engine(tr, DEV, n_ckpt=26, max_owners=50)
+    src = OffsetRows(tr, DEV)
+    log = run_trace(eng, tr, src)
+    torch.cuda.synchronize()
+    worst = max(nm.normwise_rel_err(src.out[k], ref.outputs[k]) for k in ref.outputs)
+    assert worst <= nm.TOL["bf16"], worst
+    assert log.versions == ref.versions and log.commits == ref.commits

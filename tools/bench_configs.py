@@ -86,7 +86,7 @@ class WindowInputs(InputSource):
     def step_io(self, ss, ps):
         S, C, tr = self.tr.n_streams, self.tr.chunk, self.tr
         rows = [(p % C) * S + s for s, p in zip(ss, ps)]
-        return StepIO(self.X, C * S * tr.d_ff, self.V, C * S * tr.d_model, self.Y, C * S * tr.d_model, rows)
+        return StepIO(self.X, C * S * tr.d_ff, self.V, C * S * tr.d_model, self.Y, C * S * tr.d_model, rows, C * S)
 
 
 def trace_of(name: str, warmup: int = 1):
