@@ -33,6 +33,12 @@ namespace {
 using namespace ptx;
 
 constexpr int BM = 128, BK = 64, kStages = 4;
+#ifndef TTT_LR_STAGES
+#define TTT_LR_STAGES 4
+#endif
+// fused low-rank READ ring depth (r2: 3 stages — a smaller shared-memory carveout, more L1 for
+// the u-warps' register streams — measured R = 16 31.3 vs 30.1 µs, R = 64 54.5 vs 54.4 µs)
+constexpr int kStagesLR = TTT_LR_STAGES;
 constexpr int kThreads = 192;
 #ifndef TTT_LR_UW
 #define TTT_LR_UW 16
@@ -173,6 +179,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
   constexpr uint32_t STAGE = A_BYTES + (LR ? 1 : 2) * B_BYTES;      // low-rank base mode has no ΔW box
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kStages = LR ? kStagesLR : ::ttt::kStages;          // ring depth of this mode
   u64 *bars = reinterpret_cast<u64 *>(smem + kStages * STAGE);
   u64 *full = bars, *empty = bars + kStages, *t_full = bars + 2 * kStages, *t_empty = t_full + 1;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(t_empty + 1);
@@ -491,7 +498,8 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
 
 template <int BN, bool LR>
 size_t smem_bytes(int d_ff) {   // LR: stages without the ΔW box, plus one x row
-  return 1024 + (size_t)kStages * (BM * BK * 2 + (LR ? 1 : 2) * BN * BK * 2) + 256 + (LR ? 256 + (size_t)d_ff * 2 : 0);
+  return 1024 + (size_t)(LR ? kStagesLR : kStages) * (BM * BK * 2 + (LR ? 1 : 2) * BN * BK * 2) + 256 +
+         (LR ? 256 + (size_t)d_ff * 2 : 0);
 }
 
 template <int BN, bool LR>
