@@ -343,7 +343,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2605_28053_b200 import capi
-    from paper_2605_28053_b200.serving import Engine, InputSource, Server, StepIO
+    from paper_2605_28053_b200.serving import Engine, Server
     from workload import rng
     from workload import traces as T
 
