@@ -51,3 +51,6 @@ for dff in (512, 384):
                         delta0="rng", controls={(1, 15): ["poison"], (2, 20): ["snapshot"], (2, 33): ["rollback"],
                                                 (3, 31): ["fail"]}), impl=2)
 print("sanitize smoke ok")
+# r2: SPEC-compat rule 1 WRITE and the low-rank READ fed from contiguous rows of a larger buffer
+run(T.uniform_small(n_streams=2, n_layers=1, d_model=64, d_ff=64, chunk=4, n_steps=9, dtype="fp32", rule=1))
+print("sanitize smoke ok (r2 additions)")
