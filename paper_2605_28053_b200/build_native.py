@@ -26,7 +26,7 @@ CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", f"-I{ROOT}/include", f"-I{CSR
             "-I/usr/local/cuda/include"]
 
 PRODUCT_CU = ["kernels/read_decode.cu", "kernels/write_simt.cu", "kernels/write_tc.cu",
-              "kernels/read_chunk_tc.cu", "kernels/lowrank.cu", "kernels/lowrank_tc.cu", "kernels/control.cu"]
+              "kernels/read_chunk_tc.cu", "kernels/read_chunk_wide.cu", "kernels/lowrank.cu", "kernels/lowrank_tc.cu", "kernels/control.cu"]
 PRODUCT_CPP = ["tttstate.cpp", "planner.cpp"]
 GEN_CU = ["gen/ttt_gen.cu"]
 

@@ -109,7 +109,23 @@ struct ChunkLaunch {
   int cooperative = 0;                      // fused mode: cooperative launch (several low-rank pools live)
   const int *d_members = nullptr;           // device member table [5][kMaxGroup]: owner_idx, x_row, v_row,
                                             // y_row, tail_pos (kernel params stay small: see MemberTable)
+  float *wide_slab = nullptr;               // wide split-K chunk READ: fp32 partial slabs (pool workspace)
+  size_t wide_slab_bytes = 0;
+  int *wide_tickets = nullptr;              //   and its per-tile arrival counters (zero at rest)
 };
+
+// Wide-tile split-K chunk READ plan (read_chunk_wide.cu): MPC members per CTA sharing each
+// W_down box, T N-blocks (j < h: w_hi wide, else w_hi - 32), K split KS ways, one wave.
+struct WidePlan {
+  int mpc = 0, T = 0, KS = 0, w_hi = 0, h = 0, stages = 0, stage_bytes = 0;
+  double cost = 0;               // modelled time: L2 -> SM bytes per CTA / bytes in flight
+  int tiles = 0;
+  int bk = 16;                   // K elements per ring stage (16 / 32 / 64)
+};
+constexpr int kWideMaxTiles = 160;          // workspace sizing: tiles per launch (≤ SM count)
+constexpr size_t kWideSlabBytes = (size_t)kWideMaxTiles * 512 * 128 * 4;   // 512 TMEM columns x 128 rows fp32
+bool plan_read_chunk_wide(int n, int d_model, int d_ff, int sms, int bk, WidePlan *out);
+cudaError_t launch_read_chunk_wide(const ChunkLaunch &cl, const WidePlan &pl, cudaStream_t s);
 
 // Per-member arrays of a chunk / low-rank READ group, kept in the pool's device workspace
 // instead of the kernel parameters (parameter block ~7 KB -> ~0.6 KB; host per low-rank launch

@@ -30,7 +30,6 @@
 #include "sm100_ptx.cuh"
 
 namespace ttt {
-bool cached_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1);
 
 namespace {
 

@@ -565,11 +565,13 @@ NPlan plan_n(int d_model, int tiles_per_block_unit, int sms) {
 
 // Tensor-map encode cache (host): decode-time launches reuse the same handful of maps per
 // layer, so encoding is done once per (base, dims, box).
-bool cached_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1) {
+bool cached_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
+                int swizzle_bytes) {
   struct Entry {
     const void *base;
     uint64_t d0, d1, d2;
     uint32_t b0, b1;
+    int sw;
     CUtensorMap map;
   };
   static Entry cache[128];
@@ -578,14 +580,14 @@ bool cached_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint
   std::lock_guard<std::mutex> lock(mu);
   for (int i = 0; i < n_used; ++i) {
     const Entry &e = cache[i];
-    if (e.base == base && e.d0 == d0 && e.d1 == d1 && e.d2 == d2 && e.b0 == b0 && e.b1 == b1) {
+    if (e.base == base && e.d0 == d0 && e.d1 == d1 && e.d2 == d2 && e.b0 == b0 && e.b1 == b1 && e.sw == swizzle_bytes) {
       *m = e.map;
       return true;
     }
   }
-  if (!ptx::make_map_bf16_3d(m, base, d0, d1, d2, b0, b1)) return false;
+  if (!ptx::make_map_bf16_3d(m, base, d0, d1, d2, b0, b1, swizzle_bytes)) return false;
   Entry &e = cache[next];
-  e = Entry{base, d0, d1, d2, b0, b1, *m};
+  e = Entry{base, d0, d1, d2, b0, b1, swizzle_bytes, *m};
   next = (next + 1) % 128;
   n_used = n_used < 128 ? n_used + 1 : 128;
   return true;
@@ -643,6 +645,22 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
   p.w_hi = np.w_hi;
   p.h = np.h;
   const bool fused = cl.lr != nullptr;
+  if (!fused && cl.delta && !cl.x_rowmap && !cl.Y32) {
+    // few members: the wide split-K kernel moves fewer L2 -> SM bytes per CTA (read_chunk_wide.cu)
+    // (both costs: per-CTA L2 -> SM bytes / bytes in flight, see plan_read_chunk_wide).  Opt-in
+    // (TTT_CHUNK_WIDE=1 forces it, =-1 lets the model choose): measured r2 at 8 members it is
+    // slower than this kernel at every K block (16 / 32 / 64: 163 / 125 / 162 vs 101.5 µs), see
+    // DESIGN §5 f2, so the default keeps the narrow tiles.
+    static const int wide_env = getenv("TTT_CHUNK_WIDE") ? atoi(getenv("TTT_CHUNK_WIDE")) : 0;
+    static const int wide_bk = getenv("TTT_WIDE_BK") ? atoi(getenv("TTT_WIDE_BK")) : 32;
+    WidePlan wp;
+    if (wide_env != 0 && cl.wide_slab && plan_read_chunk_wide(cl.n, cl.d_model, cl.d_ff, sms, wide_bk, &wp)) {
+      const long long waves = ((long long)cl.n * np.T + sms - 1) / sms;
+      const double stage = BM * BK * 2 + 2.0 * 160 * BK * 2;
+      const double narrow = (double)waves * cl.d_ff * 2 * (BM + 2 * np.w_hi) / ((kStages - 1) * stage);
+      if (wide_env == 1 || wp.cost < 0.95 * narrow) return launch_read_chunk_wide(cl, wp, s);
+    }
+  }
   if (fused) {
     // every tile must be resident at once: the finish waits on the other K slabs of its tile
     if (cl.n * np.T * p.ksplit > sms || cl.lr_ctr == nullptr) return cudaErrorInvalidValue;

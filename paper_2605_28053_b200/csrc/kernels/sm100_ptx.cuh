@@ -108,6 +108,29 @@ __device__ __forceinline__ u64 smem_desc_sw128(uint32_t addr, uint32_t lbo, uint
   d |= (u64)2 << 61;
   return d;
 }
+// K-major operand with RB-byte swizzled rows (RB = 128 / 64 / 32: rows of 64 / 32 / 16 bf16,
+// 8-row atoms of 8·RB bytes): layout SWIZZLE_128B = 2 / SWIZZLE_64B = 4 / SWIZZLE_32B = 6,
+// SBO = 8·RB, LBO unused for swizzled K-major operands.
+template <int RB>
+__device__ __forceinline__ u64 smem_desc_swz(uint32_t addr) {
+  static_assert(RB == 128 || RB == 64 || RB == 32, "swizzle row bytes");
+  constexpr u64 layout = RB == 128 ? 2 : RB == 64 ? 4 : 6;
+  u64 d = 0;
+  d |= (u64)((addr >> 4) & 0x3FFF);
+  d |= (u64)1 << 16;
+  d |= (u64)((8 * RB) >> 4) << 32;
+  d |= (u64)1 << 46;
+  d |= layout << 61;
+  return d;
+}
+// Plain bulk copy global -> shared (bytes % 16 == 0, both 16-B aligned), completing tx bytes
+// on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, u64 *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 // kind::f16 instruction descriptor: D fp32, A/B bf16, majors (0 = K, 1 = MN), M, N (runtime-capable).
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
@@ -175,19 +198,28 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 3-D bf16 tensor [d2][d1][d0] (d0 contiguous), box {b0, b1, 1}, 128-byte swizzle.
+// 3-D bf16 tensor [d2][d1][d0] (d0 contiguous), box {b0, b1, 1}, 128-byte swizzle
+// (swizzle_bytes 64 / 32: the 64- / 32-byte swizzle, b0 = 32 / 16).
 inline bool make_map_bf16_3d(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
-                             uint32_t b1) {
+                             uint32_t b1, int swizzle_bytes = 128) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t es[3] = {1, 1, 1};
+  const CUtensorMapSwizzle sw = swizzle_bytes == 64   ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                      : CU_TENSOR_MAP_SWIZZLE_128B;
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace ptx
+
+// Tensor-map encode cache (read_chunk_tc.cu): maps keyed by (base, dims, box, swizzle).
+bool cached_map(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
+                int swizzle_bytes = 128);
+
 }  // namespace ttt

@@ -90,6 +90,10 @@ Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt) {
   // READ partials: base K-chunk slabs [kc][8][d_model] (kc ≤ ⌈d_ff/512⌉) + ΔW [8][d_model]
   L.P = off;       off = align_up(off + ((size_t)(s.d_ff + 511) / 512 + 1) * kMaxReadMembers * s.d_model * 4, 256);
   L.tickets = off; off = align_up(off + (size_t)s.d_model * 4, 1024);
+  if (s.backend == TTT_FAST_WEIGHT && s.dtype == TTT_BF16 && s.chunk <= 128) {   // wide chunk READ (f2)
+    L.wtick = off; off = align_up(off + (size_t)kWideMaxTiles * 4, 1024);
+    L.wslab = off; off = align_up(off + kWideSlabBytes, 1024);
+  }
   if (s.backend == TTT_LOW_RANK) {
     const size_t rows = align_up((size_t)max_owners, 128);
     L.Xg = off;  off = align_up(off + rows * s.d_ff * es, 1024);
@@ -673,6 +677,11 @@ ttt_status read_apply_chunk(ttt_pool *p, const ttt_group *g, int32_t layer, cons
     CUDA_TRY(upload_members(p, mt, g->n, static_cast<cudaStream_t>(stream)));
   }
   cl.d_members = p->d_members();
+  if (p->lay.wslab) {
+    cl.wide_slab = reinterpret_cast<float *>(p->arena + p->lay.wslab);
+    cl.wide_slab_bytes = kWideSlabBytes;
+    cl.wide_tickets = reinterpret_cast<int *>(p->arena + p->lay.wtick);
+  }
   cudaError_t e = launch_read_chunk(cl, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "read_chunk launch");
   for (int b = 0; b < g->n; ++b) {

@@ -3,8 +3,9 @@ parity suites in a subprocess: the all-SIMT bf16 decode READ (used when the tens
 kernel's shared-memory staging does not fit, e.g. d_ff > 14,080), the three-launch low-rank
 READ (used when a fused launch would not fit one CTA per tile), the one-pass tcgen05 low-rank
 READ over [W_down; A] with its bulk-copy finish (TTT_LR_FUSED=2), multi-launch READ groups
-with plain loads instead of the L2 evict_last / evict_first hints (TTT_READ_L2KEEP=0), and the
-serial-order READ."""
+with plain loads instead of the L2 evict_last / evict_first hints (TTT_READ_L2KEEP=0), the
+serial-order READ, and both chunk READ kernels on every shape (TTT_CHUNK_WIDE=1 forces the wide
+split-K kernel wherever it has a plan, =0 keeps the narrow one at paper dims)."""
 import os
 import subprocess
 import sys
@@ -29,6 +30,8 @@ def _run(env_extra, target):
     ({"TTT_LR_FUSED": "0"}, "tests/test_gpu_lowrank.py"),
     ({"TTT_LR_FUSED": "2"}, "tests/test_gpu_lowrank.py"),
     ({"TTT_READ_L2KEEP": "0"}, "tests/test_gpu_configs.py"),
+    ({"TTT_CHUNK_WIDE": "1"}, "tests/test_gpu_read_chunk.py"),
+    ({"TTT_CHUNK_WIDE": "0"}, "tests/test_gpu_full_size.py::test_f2_chunk_read_paper_dims"),
 ])
 def test_alternative_paths_parity(env, target):
     _run(env, target)

@@ -47,7 +47,8 @@ def run_prefill(tr, eng):
 
 @pytest.mark.parametrize("d_model,d_ff,chunk,streams", [(320, 384, 16, 3), (256, 448, 64, 2), (384, 256, 128, 2),
                                                         (640, 512, 48, 9), (400, 320, 32, 5),
-                                                        (2560, 256, 128, 8)])
+                                                        (2560, 256, 128, 8), (2560, 1024, 128, 8),
+                                                        (1024, 2048, 100, 4)])
 def test_chunk_read_prefill_parity(d_model, d_ff, chunk, streams):
     # d_model 400 / 2560 exercise the mixed-width N blocks (25 × 16 / 16 × 144 + 2 × 128)
     tr = T.uniform_small(n_streams=streams, n_layers=2, d_model=d_model, d_ff=d_ff, chunk=chunk, n_steps=2 * chunk,
@@ -95,3 +96,13 @@ def test_chunk_read_contract_errors():
     assert e.value.status == 13 and capi.tttstate_tail_len(eng.pool, owners[0]) == tr.chunk - 1
     assert capi.write_commit(eng.pool, g, 0.01) == [1, 1]
     assert capi.tttstate_tail_len(eng.pool, owners[0]) == 0
+
+
+def test_chunk_read_deterministic():
+    """Two engines, same inputs: the chunk READ outputs are bit-identical (the wide split-K
+    kernel adds its K-slab partials in a fixed order, never by arrival)."""
+    tr = T.uniform_small(n_streams=8, n_layers=1, d_model=2560, d_ff=1024, chunk=128, n_steps=128, dtype="bf16",
+                         delta0="rng", v0=2, seed=5)
+    a = run_prefill(tr, make_engine(tr, DEV))
+    b = run_prefill(tr, make_engine(tr, DEV))
+    assert all(np.array_equal(a[k], b[k]) for k in a)
