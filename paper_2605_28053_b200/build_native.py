@@ -71,6 +71,29 @@ def _link(objs, out, force):
         raise RuntimeError(f"link failed: {out}\n{r.stdout}\n{r.stderr}")
 
 
+def build_variant(name: str, defines: list) -> str:
+    """A/B tuning build: the product library with extra -D defines, linked to
+    lib/variants/libtttstate_<name>.so (loaded with TTT_LIB_PATH; never the default)."""
+    vobj = os.path.join(OBJ, "variants", name)
+    os.makedirs(vobj, exist_ok=True)
+    out = os.path.join(LIB, "variants", f"libtttstate_{name}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    objs = []
+    for src in PRODUCT_CU + PRODUCT_CPP:
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(vobj, src.replace("/", "_") + ".o")
+        dflags = [f"-D{d}" for d in defines]
+        cmd = ([NVCC] + NVFLAGS if src.endswith(".cu") else ["g++"] + CXXFLAGS) + dflags + ["-c", path, "-o", obj]
+        objs.append((cmd, obj))
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        res = list(ex.map(lambda c: subprocess.run(c[0], capture_output=True, text=True), objs))
+    for r in res:
+        if r.returncode != 0:
+            raise RuntimeError(r.stdout + r.stderr)
+    _link([o for _, o in objs], out, True)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> dict:
     os.makedirs(LIB, exist_ok=True)
     os.makedirs(OBJ, exist_ok=True)
@@ -89,4 +112,7 @@ def build(force: bool = False, verbose: bool = False) -> dict:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":   # --variant NAME DEF=V ...
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        build(force="--force" in sys.argv, verbose=True)
