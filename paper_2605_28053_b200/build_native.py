@@ -25,7 +25,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xpt
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", f"-I{ROOT}/include", f"-I{CSRC}",
             "-I/usr/local/cuda/include"]
 
-PRODUCT_CU = ["kernels/read_decode.cu", "kernels/write_simt.cu", "kernels/write_tc.cu",
+PRODUCT_CU = ["kernels/read_decode.cu", "kernels/read_decode_tc.cu", "kernels/write_simt.cu", "kernels/write_tc.cu",
               "kernels/read_chunk_tc.cu", "kernels/read_chunk_wide.cu", "kernels/lowrank.cu", "kernels/lowrank_tc.cu", "kernels/control.cu"]
 PRODUCT_CPP = ["tttstate.cpp", "planner.cpp"]
 GEN_CU = ["gen/ttt_gen.cu"]

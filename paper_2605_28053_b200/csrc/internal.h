@@ -40,6 +40,11 @@ struct ReadParams {
   int kc;                        // > 0: tensor-core base (bf16), Pbase holds kc K-chunk slabs [kc][8][d_model]
   int l2keep;                    // not the group's last launch of this layer: keep W_down in L2 (evict_last)
   int xtma;                      // tensor-core-base kernel: stage the x rows with bulk copies (TMA)
+  // TMA + tcgen05 READ (read_decode_tc.cu): tensor-map extents and its partial-sum workspace
+  int L, layer;
+  long long n_slot_layers;       // pool slots × L (third extent of the slot tensor map)
+  float *ptc;                    // [2][g][⌈d_model/128⌉·128][8] fp32 partials
+  size_t ptc_bytes;
 };
 
 // a5: chunk update of one layer for every member (shadow slot <- ΔW_v + η VᵀZ).
@@ -180,6 +185,9 @@ bool read_chunk_supported(int d_model, int d_ff, int C);
 cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s);
 cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s);
 bool read_decode_fits(int n, int d_model, int d_ff, int esize);
+bool read_decode_tc_supported(int n, int d_model, int d_ff);
+cudaError_t launch_read_decode_tc(const ReadParams &p, cudaStream_t s);
+constexpr int kTcMaxG = 40;            // READ-tc workspace sizing: CTAs per row block
 int read_decode_mma_chunks(int dtype, int d_ff);   // > 0: the bf16 tensor-core-base READ applies (its K chunks)
 cudaError_t launch_write_simt(int dtype, const WriteParams &p, cudaStream_t s);
 cudaError_t launch_write_rule1(int dtype, const WriteParams &p, cudaStream_t s);   // SPEC-compat rule 1 (square)

@@ -777,6 +777,11 @@ cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist_mb << 20);
     limit_set = true;
   }
+  if (p.kc > 0 && !p.fuse && p.ptc && read_decode_tc_supported(p.n, p.d_model, p.d_ff)) {
+    ReadParams q = p;
+    q.l2keep = p.l2keep && l2keep;
+    return launch_read_decode_tc(q, s);            // TMA + tcgen05 (read_decode_tc.cu)
+  }
   if (p.kc > 0) {
     if (p.l2keep && l2keep) return p.fuse ? launch_mma<true, true>(p, s) : launch_mma<false, true>(p, s);
     return p.fuse ? launch_mma<true, false>(p, s) : launch_mma<false, false>(p, s);

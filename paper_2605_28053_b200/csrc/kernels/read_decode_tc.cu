@@ -1,0 +1,438 @@
+// a3 + a4 — decode READ on TMA + tcgen05 (bf16, up to 8 members per launch).
+//
+// PAPER: READ = ApplyState + ReturnOutputs (Table 3, §4.2): for every
+// member b of a legal READ group, y_b = x_b·(W_down[l] + ΔW_b[l])ᵀ, the committed slot chosen
+// by the device active-slot table, the pool never written; TailBufferUpdate appends (z_t, v_t)
+// (P:382-385).  Same operation as read_decode.cu's kernels; this one moves the bytes
+// differently.
+//
+// Why: the operation is a pure HBM stream (448.7 MB per launch at 8 members, AI ≈ 2).  A probe
+// of TMA tensor boxes into a shared-memory ring (tools/tma_tensor_probe.cu, r2) streams that
+// volume at 6.80–6.83 TB/s with two warps per SM when the boxes are dealt evenly, vs ~6.0 TB/s
+// for the 1024-thread register-batch kernel, whose warps run out of rows at different times.
+// So: every weight byte arrives as a 128-row × 64-column box (16 KB, 128-byte swizzle) and the
+// tensor core does the products — the weight rows are the MMA's A operand (M = 128) and the
+// members' x rows its B operand (N = 16: 8 member rows + 8 zero rows), accumulating
+// D[128 rows × 16] in TMEM.  For a ΔW_b box only column b of D is wanted (15/16 of that MMA is
+// thrown away — a few % of the tensor pipe, irrelevant next to the HBM stream).
+//
+// Work split: the 9 matrices (W_down, ΔW_0 … ΔW_7) × ⌈d_model/128⌉ row blocks are dealt to G
+// groups of g CTAs; CTA `sub` of a group streams K blocks [sub·nkb/g, (sub+1)·nkb/g) of each of
+// its group's row blocks, so its slice of the x rows (8 rows × its K range) is staged in shared
+// memory once.  g is chosen to balance K blocks per CTA (g = 4 at paper dims: 37 groups, 38 K
+// blocks of 64 per row block).  Each (row block, K slice) partial goes to a workspace slab; the
+// last of the (1+n)·g arrivals for an output row block (per-row-block ticket) sums, in a fixed
+// order, Σ_slices W-partial[b] + Σ_slices ΔW_b-partial (+ resid) → bf16 y (deterministic).
+// Warps: 0 TMA producer (lane 0), 1 MMA issuer (lane 0), 2–5 x staging / tail append /
+// epilogue (tcgen05.ld) / combine.  TMEM: two 16-column accumulators (row block k in k & 1).
+//
+// Measured r2 (parity-green, NOT the default — TTT_READ_TC=1 selects it): 82.8 µs per launch in
+// tools/microbench.py vs 76.3 µs for read_decode_mma_kernel on the same box; ncu (serialised,
+// cold) 84.5 vs 80.0 µs.  Per-CTA phase stamps (tools/dtc_trace.py): the streaming phase runs
+// at ~43 GB/s per SM (70 µs for 190 boxes) instead of the probe's 46 GB/s — a ring slot is held
+// until its MMAs retire; more stages (8 → 12) did not help — plus 2–4 µs of x staging per launch
+// (it was 9 µs with 128-B TMA one-row boxes: a fixed cost per tiny box), the 4.86-vs-5 row-block
+// imbalance at g = 4, and no work to overlap the PDL wait beyond the first W boxes.  It does run
+// at full clock (1,965 MHz, ~920 W) where the SIMT kernel sits at the 1 kW cap.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "../internal.h"
+#include "sm100_ptx.cuh"
+
+namespace ttt {
+namespace {
+
+using namespace ptx;
+
+constexpr int kTcThreads = 192;
+constexpr int kTcBK = 64;                          // K elements per box (128 B rows)
+constexpr int kTcBoxBytes = 128 * kTcBK * 2;       // 16 KB
+constexpr int kTcMaxStages = 12;
+
+struct DecTcParams {
+  int n, d_model, d_ff, L, layer;
+  int g, G, nkb, nrb, n_mat, stages;
+  int l2keep;
+  const int *sel;
+  const void *X, *Vt, *resid;
+  void *Y;
+  void *tailZ, *tailV;
+  long long tz_owner, tv_owner, tz_layer, tv_layer;
+  float *Pw;                     // [g][nrb·128][8]   W_down partials per K slice
+  float *Pd;                     // [g][nrb·128][8]   ΔW_b partials (column b of record b)
+  int *tickets;                  // [nrb] arrivals per output row block (self-resetting)
+  int owner_idx[kMaxReadMembers], x_row[kMaxReadMembers], v_row[kMaxReadMembers], y_row[kMaxReadMembers];
+  int tail_pos[kMaxReadMembers];
+  int trace;                     // TTT_READ_TC_TRACE=1: per-CTA %globaltimer stamps printed at exit
+  int pre;                       // W boxes requested before the PDL wait
+};
+
+template <int ID, int COUNT>
+__device__ __forceinline__ void named_bar() {
+  asm volatile("barrier.sync %0, %1;" ::"n"(ID), "n"(COUNT) : "memory");
+}
+// 32 lanes × 8 consecutive 32-bit TMEM columns
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    read_decode_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmD,
+                          const DecTcParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = p.stages, g = p.g, grp = blockIdx.x / g, sub = blockIdx.x - grp * g;
+  const int kb_lo = sub * p.nkb / g, kb_hi = (sub + 1) * p.nkb / g, nkq = kb_hi - kb_lo;
+  unsigned char *xs = smem + (size_t)S * kTcBoxBytes;          // [nkq][8 rows][128 B] swizzled x slice
+  u64 *bars = reinterpret_cast<u64 *>(xs + (size_t)nkq * 1024);
+  u64 *full = bars, *empty = bars + kTcMaxStages, *t_full = bars + 2 * kTcMaxStages, *t_empty = t_full + 2;
+  u64 *x_ready = t_empty + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(x_ready + 1);
+  __shared__ int s_last;
+  __shared__ unsigned long long ts[7];
+  auto stamp = [&](int i) {
+    if (p.trace) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[i] = t;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_rb = p.n_mat * p.nrb;                              // row blocks over all matrices
+  const int my_rbs = grp < p.G ? (n_rb - grp + p.G - 1) / p.G : 0;
+  auto rb_of = [&](int k, int &m, int &rbi) {                    // k-th row block of this group
+    const int r = grp + k * p.G;
+    m = r / p.nrb;
+    rbi = r - m * p.nrb;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(t_full + i, 1);
+      mbar_init(t_empty + i, 4);
+    }
+    mbar_init(x_ready, 128);                          // every warp-2..5 thread
+    mbar_init_fence();
+  }
+  if (warp == 1) tmem_alloc<32>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  asm volatile("griddepcontrol.launch_dependents;");
+
+  if (warp == 0) {
+    if (lane == 0 && my_rbs > 0) {                          // ---------------- TMA producer
+      tma_prefetch(&tmW);
+      tma_prefetch(&tmD);
+      const u64 pol_w = p.l2keep ? policy_evict_last() : 0ull;
+      int it = 0;
+      // W_down is never written by any kernel: this group's W boxes may be requested before the
+      // PDL wait (ΔW boxes need the slot table, written by commits)
+      bool waited = false;
+      for (int k = 0; k < my_rbs; ++k) {
+        int m, rbi;
+        rb_of(k, m, rbi);
+        int coord2 = p.layer;
+        if (m > 0) {
+          if (!waited) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            waited = true;
+          }
+          const int o = p.owner_idx[m - 1];
+          coord2 = (2 * o + p.sel[o]) * p.L + p.layer;
+        }
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
+          const int s = it % S;
+          if (it >= p.pre || it >= S) {
+            if (!waited) {                                   // (pre-wait prefetch budget used: wait now)
+              asm volatile("griddepcontrol.wait;" ::: "memory");
+              waited = true;
+            }
+            mbar_wait(empty + s, ((it / S) - 1) & 1);
+          }
+          mbar_expect_tx(full + s, kTcBoxBytes);
+          unsigned char *dst = smem + (size_t)s * kTcBoxBytes;
+          if (m == 0) {
+            if (p.l2keep) tma_load_3d_hint(dst, &tmW, full + s, kb * kTcBK, rbi * 128, 0, pol_w);
+            else tma_load_3d(dst, &tmW, full + s, kb * kTcBK, rbi * 128, 0);
+          } else {
+            tma_load_3d(dst, &tmD, full + s, kb * kTcBK, rbi * 128, coord2);
+          }
+        }
+      }
+      if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
+  } else if (warp == 1) {                                   // ---------------- MMA issuer
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (my_rbs > 0) {
+      mbar_wait(x_ready, 0);
+      if (lane == 0) stamp(1);
+      tc_fence_after();
+      // N = 16: B rows 8..15 alias rows 0..7 (SBO = 0), i.e. D columns 8..15 repeat 0..7 (unused)
+      const uint32_t idesc = idesc_bf16(128, 16, 0, 0);
+      const uint32_t xb0 = smem_u32(xs);
+      int it = 0;
+      for (int k = 0; k < my_rbs; ++k) {
+        const uint32_t acc = tmem + (uint32_t)((k & 1) * 16);
+        if (k >= 2) {
+          mbar_wait(t_empty + (k & 1), ((k >> 1) - 1) & 1);
+          tc_fence_after();
+        }
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
+          const int s = it % S;
+          mbar_wait(full + s, (it / S) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(smem + (size_t)s * kTcBoxBytes), b0 = xb0 + (uint32_t)(kb - kb_lo) * 1024;
+#pragma unroll
+            for (int kk = 0; kk < kTcBK / 16; ++kk)
+              mma_bf16(acc, smem_desc_sw128(a0 + kk * 32, 16, 1024), smem_desc_sw128(b0 + kk * 32, 16, 0), idesc,
+                       (kb > kb_lo || kk > 0) ? 1u : 0u);
+            mma_commit(empty + s);
+            if (kb == kb_hi - 1) mma_commit(t_full + (k & 1));
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {                                                  // ---------------- warps 2-5
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 64) stamp(5);
+    const int q = warp & 3, et = threadIdx.x - 64;
+    const int n = p.n, dff = p.d_ff, dm = p.d_model;
+    if (my_rbs > 0) {
+      // x slice → shared memory, K-major 128-byte-swizzled 8-row atoms: 16-B chunk c of row r in
+      // atom kbl at kbl·1024 + r·128 + ((c ^ r)·16); rows n..7 zero.  Plain 16-B loads, all of a
+      // thread's chunks in flight at once (one round trip; TMA one-row boxes took ~9 µs here: a
+      // fixed cost per tiny box), then fence.proxy.async so the MMA (async proxy) sees them.
+      constexpr int kXPer = 24;
+      const int chunks = nkq * 64;
+      for (int i0 = et; i0 < chunks; i0 += 128 * kXPer) {
+        uint4 v[kXPer];
+#pragma unroll
+        for (int u = 0; u < kXPer; ++u) {
+          const int i = i0 + u * 128, kbl = i >> 6, r = (i >> 3) & 7, c = i & 7;
+          const int kel = (kb_lo + kbl) * kTcBK + c * 8;
+          v[u] = make_uint4(0u, 0u, 0u, 0u);
+          if (i < chunks && r < n && kel < dff)
+            v[u] = *reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[r] * dff +
+                                                    kel);
+        }
+#pragma unroll
+        for (int u = 0; u < kXPer; ++u) {
+          const int i = i0 + u * 128, kbl = i >> 6, r = (i >> 3) & 7, c = i & 7;
+          if (i < chunks) *reinterpret_cast<uint4 *>(xs + (size_t)kbl * 1024 + r * 128 + ((c ^ r) << 4)) = v[u];
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes → MMA (async proxy)
+      mbar_arrive(x_ready);
+    }
+    {                                                       // a4 — TailBufferUpdate, spread over every CTA
+      const int zq = n * (dff / 8), gtid = blockIdx.x * 128 + et, gsz = gridDim.x * 128;
+      for (int idx = gtid; idx < zq; idx += gsz) {
+        const int b = idx / (dff / 8), vv = idx - b * (dff / 8), o = p.owner_idx[b];
+        reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.tailZ) + o * p.tz_owner + p.tz_layer +
+                                  (size_t)p.tail_pos[b] * dff)[vv] =
+            reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff)[vv];
+      }
+      for (int idx = gtid; idx < n * dm; idx += gsz) {
+        const int b = idx / dm, ii = idx - b * dm, o = p.owner_idx[b];
+        (static_cast<__nv_bfloat16 *>(p.tailV) + o * p.tv_owner + p.tv_layer + (size_t)p.tail_pos[b] * dm)[ii] =
+            (static_cast<const __nv_bfloat16 *>(p.Vt) + (size_t)p.v_row[b] * dm)[ii];
+      }
+    }
+    const int rows_pad = p.nrb * 128;
+    for (int k = 0; k < my_rbs; ++k) {
+      int m, rbi;
+      rb_of(k, m, rbi);
+      mbar_wait(t_full + (k & 1), (k >> 1) & 1);
+      if (et == 0 && k == 0) stamp(2);
+      tc_fence_after();
+      uint32_t r[8];
+      tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((k & 1) * 16), r);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(t_empty + (k & 1));
+      const int row = rbi * 128 + q * 32 + lane;           // < rows_pad; rows ≥ d_model are zero boxes
+      if (m == 0) {                                         // W_down partial: all 8 member columns
+        float4 *d4 = reinterpret_cast<float4 *>(p.Pw + ((size_t)sub * rows_pad + row) * 8);
+        __stcg(d4, make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3])));
+        __stcg(d4 + 1, make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]), __uint_as_float(r[7])));
+      } else {                                              // ΔW_b partial: column b only, same record layout
+        const int b = m - 1;
+        float v = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (e == b) v = __uint_as_float(r[e]);
+        __stcg(p.Pd + ((size_t)sub * rows_pad + row) * 8 + b, v);
+      }
+      named_bar<1, 128>();                                  // the row block's partials are stored
+      if (et == 0) {
+        __threadfence();
+        s_last = atomicAdd(p.tickets + rbi, 1) == p.n_mat * g - 1;
+      }
+      named_bar<1, 128>();
+      if (s_last) {                                         // combine output row block rbi (fixed order)
+        __threadfence();
+        const int i = rbi * 128 + et;
+        if (i < dm) {
+          // y_b = Σ_slices W-partial[b] + Σ_slices ΔW_b-partial, slices ascending; the loads of
+          // four slices are issued together (one L2 round trip per four slices)
+          float w[8], d[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) w[e] = d[e] = 0.f;
+          for (int s0 = 0; s0 < g; s0 += 4) {
+            float4 lw[4][2], ld[4][2];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const bool ok = s0 + u < g;
+              const float4 *pw = reinterpret_cast<const float4 *>(p.Pw + ((size_t)(s0 + u) * rows_pad + i) * 8);
+              const float4 *pd = reinterpret_cast<const float4 *>(p.Pd + ((size_t)(s0 + u) * rows_pad + i) * 8);
+              const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+              lw[u][0] = ok ? __ldcg(pw) : z;
+              lw[u][1] = ok ? __ldcg(pw + 1) : z;
+              ld[u][0] = ok ? __ldcg(pd) : z;
+              ld[u][1] = ok ? __ldcg(pd + 1) : z;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (s0 + u >= g) break;
+              w[0] += lw[u][0].x; w[1] += lw[u][0].y; w[2] += lw[u][0].z; w[3] += lw[u][0].w;
+              w[4] += lw[u][1].x; w[5] += lw[u][1].y; w[6] += lw[u][1].z; w[7] += lw[u][1].w;
+              d[0] += ld[u][0].x; d[1] += ld[u][0].y; d[2] += ld[u][0].z; d[3] += ld[u][0].w;
+              d[4] += ld[u][1].x; d[5] += ld[u][1].y; d[6] += ld[u][1].z; d[7] += ld[u][1].w;
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            if (b >= n) break;
+            float y = w[b] + d[b];
+            if (p.resid)
+              y += __bfloat162float(static_cast<const __nv_bfloat16 *>(p.resid)[(size_t)p.y_row[b] * dm + i]);
+            static_cast<__nv_bfloat16 *>(p.Y)[(size_t)p.y_row[b] * dm + i] = __float2bfloat16_rn(y);
+          }
+        }
+        if (et == 0) p.tickets[rbi] = 0;                    // self-reset for the next launch
+      }
+    }
+  }
+  if (threadIdx.x == 64) stamp(3);
+  tc_fence_before();
+  __syncwarp();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<32>(tmem);
+  if (p.trace && threadIdx.x == 0) {
+    stamp(4);
+    printf("DTC %d %llu %llu %llu %llu %llu %d %llu\n", (int)blockIdx.x, ts[0], ts[1], ts[2], ts[3], ts[4], p.layer,
+           ts[5]);
+  }
+}
+
+// g (CTAs per row block) minimising the K blocks of the busiest CTA, ⌈rbs / G⌉ · ⌈nkb / g⌉;
+// among equals the smallest x slice (8 rows × its K blocks × 128 B), which leaves the most ring
+// stages: a box's slot is held until its MMAs complete, so bytes in flight = ring − slots in MMA.
+int plan_g(int n_rb, int nkb, int sms, int *G_out, int *stages_out) {
+  int best = 0, best_cost = 1 << 30, best_st = 0;
+  static const int st_env = getenv("TTT_READ_TC_STAGES") ? atoi(getenv("TTT_READ_TC_STAGES")) : kTcMaxStages;
+  for (int g = 1; g <= std::min(sms, nkb); ++g) {
+    const int G = sms / g, nkq = (nkb + g - 1) / g;
+    const int st = std::min(st_env, (int)((227 * 1024 - 4096 - (size_t)nkq * 1024) / kTcBoxBytes));
+    if (st < 4) continue;
+    const int cost = ((n_rb + G - 1) / G) * nkq;
+    if (cost < best_cost || (cost == best_cost && st > best_st)) {
+      best_cost = cost;
+      best = g;
+      best_st = st;
+    }
+  }
+  if (best) {
+    *G_out = sms / best;
+    *stages_out = best_st;
+  }
+  return best;
+}
+
+}  // namespace
+
+bool read_decode_tc_supported(int n, int d_model, int d_ff) {
+  static const int on = getenv("TTT_READ_TC") ? atoi(getenv("TTT_READ_TC")) : 0;   // opt-in (see header)
+  return on && n >= 1 && n <= kMaxReadMembers && d_model >= 128 && d_ff % 8 == 0 && d_ff >= kTcBK &&
+         ptx::encode_fn() != nullptr;
+}
+
+cudaError_t launch_read_decode_tc(const ReadParams &rp, cudaStream_t s) {
+  DecTcParams p{};
+  p.n = rp.n; p.d_model = rp.d_model; p.d_ff = rp.d_ff; p.L = rp.L; p.layer = rp.layer;
+  p.nkb = (rp.d_ff + kTcBK - 1) / kTcBK;
+  p.nrb = (rp.d_model + 127) / 128;
+  p.n_mat = 1 + rp.n;
+  const int sms = device_sm_count();
+  p.g = plan_g(p.n_mat * p.nrb, p.nkb, sms, &p.G, &p.stages);
+  static const int g_env = getenv("TTT_READ_TC_G") ? atoi(getenv("TTT_READ_TC_G")) : 0;
+  if (g_env > 0 && g_env <= sms) {                 // tuning override
+    p.g = g_env;
+    p.G = sms / g_env;
+    const int nkq_e = (p.nkb + p.g - 1) / p.g;
+    p.stages = std::min(kTcMaxStages, (int)((227 * 1024 - 4096 - (size_t)nkq_e * 1024) / kTcBoxBytes));
+  }
+  if (p.g == 0 || (size_t)p.g * p.nrb * 128 * 8 * 2 * sizeof(float) > rp.ptc_bytes) return cudaErrorInvalidValue;
+  p.l2keep = rp.l2keep;
+  static const int trace = getenv("TTT_READ_TC_TRACE") ? atoi(getenv("TTT_READ_TC_TRACE")) : 0;
+  p.trace = trace;
+  static const int pre = getenv("TTT_READ_TC_PRE") ? atoi(getenv("TTT_READ_TC_PRE")) : 1 << 20;
+  p.pre = pre;
+  p.sel = rp.sel;
+  p.X = rp.X; p.Vt = rp.Vt; p.resid = rp.resid; p.Y = rp.Y;
+  p.tailZ = rp.tailZ; p.tailV = rp.tailV;
+  p.tz_owner = rp.tz_owner; p.tv_owner = rp.tv_owner; p.tz_layer = rp.tz_layer; p.tv_layer = rp.tv_layer;
+  p.Pw = rp.ptc;
+  p.Pd = rp.ptc + (size_t)p.g * p.nrb * 128 * 8;
+  p.tickets = rp.tickets;
+  for (int b = 0; b < rp.n; ++b) {
+    p.owner_idx[b] = rp.owner_idx[b];
+    p.x_row[b] = rp.x_row[b];
+    p.v_row[b] = rp.v_row[b];
+    p.y_row[b] = rp.y_row[b];
+    p.tail_pos[b] = rp.tail_pos[b];
+  }
+  CUtensorMap mW, mD;
+  if (!cached_map(&mW, rp.w_down_l, rp.d_ff, rp.d_model, 1, kTcBK, 128) ||
+      !cached_map(&mD, rp.slots, rp.d_ff, rp.d_model, (uint64_t)rp.n_slot_layers, kTcBK, 128))
+    return cudaErrorInvalidValue;
+  const int nkq = (p.nkb + p.g - 1) / p.g;
+  const size_t smem = 1024 + (size_t)p.stages * kTcBoxBytes + (size_t)nkq * 1024 + (2 * kTcMaxStages + 6) * 8 + 16;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(read_decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  static const bool pdl = !getenv("TTT_PDL") || atoi(getenv("TTT_PDL")) != 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, read_decode_tc_kernel, mW, mD, p);
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+}  // namespace ttt

@@ -34,6 +34,7 @@ struct Layout {
   size_t slots = 0, tailZ = 0, tailV = 0, sel = 0, ver = 0, flags = 0, mfail = 0, rlog = 0, P = 0, tickets = 0;
   size_t members = 0;                              // MemberTable (chunk / low-rank READ groups)
   size_t wslab = 0, wtick = 0;                     // wide split-K chunk READ workspace (bf16 fast-weight)
+  size_t ptc = 0, ptc_bytes = 0;                   // TMA + tcgen05 decode READ partials (bf16 fast-weight)
   size_t Xg = 0, Y32 = 0, U = 0, Ctr = 0, total = 0;   // low-rank READ workspace
 };
 

@@ -90,6 +90,10 @@ Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt) {
   // READ partials: base K-chunk slabs [kc][8][d_model] (kc ≤ ⌈d_ff/512⌉) + ΔW [8][d_model]
   L.P = off;       off = align_up(off + ((size_t)(s.d_ff + 511) / 512 + 1) * kMaxReadMembers * s.d_model * 4, 256);
   L.tickets = off; off = align_up(off + (size_t)s.d_model * 4, 1024);
+  if (s.backend == TTT_FAST_WEIGHT && s.dtype == TTT_BF16) {                     // decode READ on tcgen05
+    L.ptc_bytes = (size_t)2 * kTcMaxG * ((s.d_model + 127) / 128 * 128) * 8 * 4;
+    L.ptc = off; off = align_up(off + L.ptc_bytes, 1024);
+  }
   if (s.backend == TTT_FAST_WEIGHT && s.dtype == TTT_BF16 && s.chunk <= 128) {   // wide chunk READ (f2)
     L.wtick = off; off = align_up(off + (size_t)kWideMaxTiles * 4, 1024);
     L.wslab = off; off = align_up(off + kWideSlabBytes, 1024);
@@ -587,6 +591,11 @@ ttt_status read_apply_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec
       rp.y_row[k] = y_rows ? y_rows[b] : b;
       rp.tail_pos[k] = recs[b]->tail_len;
     }
+    rp.L = sh.n_layers;
+    rp.layer = layer;
+    rp.n_slot_layers = (long long)(2 * p->max_owners + p->n_ckpt) * sh.n_layers;
+    rp.ptc = p->lay.ptc_bytes ? reinterpret_cast<float *>(p->arena + p->lay.ptc) : nullptr;
+    rp.ptc_bytes = p->lay.ptc_bytes;
     cudaError_t e = launch_read_decode(sh.dtype, rp, s);
     if (e != cudaSuccess) return cuda_fail(e, "read_decode launch");
   }
