@@ -67,6 +67,7 @@ struct DecTcParams {
   int tail_pos[kMaxReadMembers];
   int trace;                     // TTT_READ_TC_TRACE=1: per-CTA %globaltimer stamps printed at exit
   int pre;                       // W boxes requested before the PDL wait
+  int nomma;                     // diagnostic: release ring slots without MMAs (wrong results)
 };
 
 template <int ID, int COUNT>
@@ -194,7 +195,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const int s = it % S;
           mbar_wait(full + s, (it / S) & 1);
           tc_fence_after();
-          if (lane == 0) {
+          if (lane == 0 && p.nomma) {                       // diagnostic (TTT_READ_TC_NOMMA): stream only
+            mbar_arrive(empty + s);
+            if (kb == kb_hi - 1) mbar_arrive(t_full + (k & 1));
+          } else if (lane == 0) {
             const uint32_t a0 = smem_u32(smem + (size_t)s * kTcBoxBytes), b0 = xb0 + (uint32_t)(kb - kb_lo) * 1024;
 #pragma unroll
             for (int kk = 0; kk < kTcBK / 16; ++kk)
@@ -393,6 +397,8 @@ cudaError_t launch_read_decode_tc(const ReadParams &rp, cudaStream_t s) {
   p.trace = trace;
   static const int pre = getenv("TTT_READ_TC_PRE") ? atoi(getenv("TTT_READ_TC_PRE")) : 1 << 20;
   p.pre = pre;
+  static const int nomma = getenv("TTT_READ_TC_NOMMA") ? atoi(getenv("TTT_READ_TC_NOMMA")) : 0;
+  p.nomma = nomma;
   p.sel = rp.sel;
   p.X = rp.X; p.Vt = rp.Vt; p.resid = rp.resid; p.Y = rp.Y;
   p.tailZ = rp.tailZ; p.tailV = rp.tailV;
