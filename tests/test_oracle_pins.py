@@ -202,6 +202,40 @@ def test_state_contract_spec_examples():
     assert tab.version(99) == 2 and tab.version(1) == 1 and np.array_equal(tab.owners[1].S[0], snap)
 
 
+def test_rollback_mid_chunk_and_fork_contents():
+    """Reading vii (rollback clears the tail: the rolled-back chunk's evidence is discarded) and
+    reading viii (a fork carries the committed state at the same version, empty tail; S:113,
+    S:145): checked by the values they imply, with dyadic inputs so every sum is exact."""
+    eta = 0.5
+    tab = StateTable(1, 2, 3, 2, "fp32", [np.zeros((2, 3))], eta)      # C = 2
+    init = [np.array([[1.0, 0.0, -1.0], [0.5, 2.0, 0.0]])]
+    tab.alloc(1, init=init, v0=3)
+    tab.snapshot(1)
+    z1, v1 = np.array([1.0, 2.0, 0.0]), np.array([1.0, -1.0])
+    tab.apply(1, 0, [z1], [v1])                                          # half a chunk of evidence
+    assert tab.tail_len(1) == 1
+    assert tab.rollback(1) == 3 and tab.tail_len(1) == 0                 # reading vii: evidence dropped
+    assert tab.next_effect(1) == READ                                    # a full new chunk is needed
+    z2, v2 = np.array([0.0, 1.0, 1.0]), np.array([2.0, 0.0])
+    z3, v3 = np.array([1.0, 0.0, 0.5]), np.array([0.0, 1.0])
+    tab.apply(1, 1, [z2], [v2])
+    assert tab.next_effect(1) == WRITE
+    tab.apply(1, 2, [z3], [v3])
+    assert tab.write_group([1]) == [4]
+    expect = init[0] + eta * (np.outer(v2, z2) + np.outer(v3, z3))   # z1's evidence absent
+    assert np.array_equal(tab.owners[1].S[0], expect)
+    # fork: same committed bytes and version, empty tail; its READ equals the source's
+    assert tab.fork(1, 7) == 4 and tab.version(7) == 4 and tab.tail_len(7) == 0
+    assert np.array_equal(tab.owners[7].S[0], expect)
+    y_src = tab.apply(1, 3, [z1], [v1])[0]
+    y_fork = tab.apply(7, 0, [z1], [v1])[0]
+    assert np.array_equal(y_src, y_fork) and np.array_equal(y_fork, expect @ z1)
+    tab.apply(7, 1, [z2], [v2])
+    assert tab.write_group([7]) == [5]
+    assert np.array_equal(tab.owners[7].S[0], expect + eta * (np.outer(v1, z1) + np.outer(v2, z2)))
+    assert np.array_equal(tab.owners[1].S[0], expect) and tab.version(1) == 4   # isolation (S:117)
+
+
 def test_group_write_is_atomic_and_owner_local():
     tab = _tiny_table()
     for r in (1, 2, 3):
@@ -317,6 +351,26 @@ def test_planner_rejects_stale_and_collisions_and_allows_mixed_versions():
     assert validate_group(g[0], V, [1, 4]) == "VERSION_MISMATCH"
 
 
+def test_planner_rejects_waiting_event_after_commit_behind_its_back():
+    """S:301 (a version mismatch is rejected to revalidation, never silently issued) and S:314
+    ("commit behind the event's back, then validate"): an event that matched V(r) on arrival and
+    is still waiting in its bucket is rejected once a commit moves V(r); the others still issue
+    when the wait budget runs out (Eq. 4)."""
+    V = {1: 0, 2: 0}
+    p = OraclePlanner(8, 4)                               # B = 8, w = 4: two events wait
+    g, rej = p.plan([_ev(1, v=0, ready=0), _ev(2, v=0, ready=0)], 0, V.get)
+    assert not g and not rej
+    V[1] = 1                                              # owner 1 commits behind its event's back
+    g, rej = p.plan([], 1, V.get)
+    assert [e.owner for e in rej] == [1] and not g
+    issued = []
+    for clock in range(2, 8):
+        g, rej = p.plan([], clock, V.get)
+        assert not rej
+        issued += [(grp.owners, grp.issue_step) for grp in g]
+    assert issued == [([2], 4)]
+
+
 def test_planner_property_eq3_eq4_random():
     """≥1000 random event sets: homogeneous κ, injective μ, version match, bounded wait."""
     rs = np.random.default_rng(7)
@@ -350,6 +404,18 @@ def test_planner_property_eq3_eq4_random():
                 for r in g.owners:
                     waiting.pop(r)
         assert not waiting
+
+
+def test_storage_rounding_goes_through_fp32():
+    """Reading xi (SURVEY §8(c) xi): bf16 storage is one RNE of the fp32 accumulator
+    value, so a candidate just above a bf16 tie whose excess is below fp32 resolution rounds as
+    the tie does (to even).  Pinned to torch's fp64 -> fp32 -> bf16 conversions (library RNE)."""
+    x = np.array([1 + 2**-8 + 2**-30, -(1 + 3 * 2**-8 + 2**-30), 1 + 2**-8 + 2**-20, 3 * 2**-130 + 2**-160])
+    ref = torch.tensor(x, dtype=torch.float64).to(torch.float32).to(torch.bfloat16).to(torch.float64).numpy()
+    got = nm.to_storage(x, "bf16")
+    assert np.array_equal(got, ref), (got, ref)
+    assert got[0] == 1.0                                  # a direct fp64 -> bf16 RNE gives 1 + 2**-7
+    assert got[2] == 1 + 2**-7
 
 
 def test_normwise_metric():
