@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     mbar_init(x_ready, 128);                          // every warp-2..5 thread
     mbar_init_fence();
   }
-  if (warp == 1) tmem_alloc<32>(tmem_slot);
+  if (warp == 1) tmem_alloc<128>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const uint32_t xb0 = smem_u32(xs);
       int it = 0;
       for (int k = 0; k < my_rbs; ++k) {
-        const uint32_t acc = tmem + (uint32_t)((k & 1) * 16);
+        const uint32_t acc = tmem + (uint32_t)((k & 1) * 64);   // 4 accumulators of 16 columns (one per K=16 step)
         if (k >= 2) {
           mbar_wait(t_empty + (k & 1), ((k >> 1) - 1) & 1);
           tc_fence_after();
@@ -202,8 +202,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const uint32_t a0 = smem_u32(smem + (size_t)s * kTcBoxBytes), b0 = xb0 + (uint32_t)(kb - kb_lo) * 1024;
 #pragma unroll
             for (int kk = 0; kk < kTcBK / 16; ++kk)
-              mma_bf16(acc, smem_desc_sw128(a0 + kk * 32, 16, 1024), smem_desc_sw128(b0 + kk * 32, 16, 0), idesc,
-                       (kb > kb_lo || kk > 0) ? 1u : 0u);
+              mma_bf16(acc + kk * 16, smem_desc_sw128(a0 + kk * 32, 16, 1024), smem_desc_sw128(b0 + kk * 32, 16, 0),
+                       idesc, kb > kb_lo ? 1u : 0u);
             mma_commit(empty + s);
             if (kb == kb_hi - 1) mma_commit(t_full + (k & 1));
           }
@@ -265,7 +265,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (et == 0 && k == 0) stamp(2);
       tc_fence_after();
       uint32_t r[8];
-      tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((k & 1) * 16), r);
+      {   // the 4 independent accumulator chains (a dependent chain of N = 16 MMAs was latency-bound),
+          // summed in a fixed order
+        const uint32_t t0 = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((k & 1) * 64);
+        uint32_t r1[8], r2[8], r3[8];
+        tmem_ld8(t0, r);
+        tmem_ld8(t0 + 16, r1);
+        tmem_ld8(t0 + 32, r2);
+        tmem_ld8(t0 + 48, r3);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          r[e] = __float_as_uint(((__uint_as_float(r[e]) + __uint_as_float(r1[e])) + __uint_as_float(r2[e])) +
+                                 __uint_as_float(r3[e]));
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(t_empty + (k & 1));
@@ -336,7 +348,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_before();
   __syncwarp();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<32>(tmem);
+  if (warp == 1) tmem_dealloc<128>(tmem);
   if (p.trace && threadIdx.x == 0) {
     stamp(4);
     printf("DTC %d %llu %llu %llu %llu %llu %d %llu\n", (int)blockIdx.x, ts[0], ts[1], ts[2], ts[3], ts[4], p.layer,
