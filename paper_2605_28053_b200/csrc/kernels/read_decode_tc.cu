@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 int plan_g(int n_rb, int nkb, int sms, int *G_out, int *stages_out) {
   int best = 0, best_cost = 1 << 30, best_st = 0;
   static const int st_env = getenv("TTT_READ_TC_STAGES") ? atoi(getenv("TTT_READ_TC_STAGES")) : kTcMaxStages;
-  for (int g = 1; g <= std::min(sms, nkb); ++g) {
+  for (int g = 1; g <= std::min({sms, nkb, kTcMaxG}); ++g) {     // (kTcMaxG: the partials workspace)
     const int G = sms / g, nkq = (nkb + g - 1) / g;
     const int st = std::min(st_env, (int)((227 * 1024 - 4096 - (size_t)nkq * 1024) / kTcBoxBytes));
     if (st < 4) continue;
@@ -397,7 +397,7 @@ cudaError_t launch_read_decode_tc(const ReadParams &rp, cudaStream_t s) {
   const int sms = device_sm_count();
   p.g = plan_g(p.n_mat * p.nrb, p.nkb, sms, &p.G, &p.stages);
   static const int g_env = getenv("TTT_READ_TC_G") ? atoi(getenv("TTT_READ_TC_G")) : 0;
-  if (g_env > 0 && g_env <= sms) {                 // tuning override
+  if (g_env > 0 && g_env <= std::min(sms, kTcMaxG)) {   // tuning override
     p.g = g_env;
     p.G = sms / g_env;
     const int nkq_e = (p.nkb + p.g - 1) / p.g;
