@@ -40,6 +40,7 @@ struct ReadParams {
   int kc;                        // > 0: tensor-core base (bf16), Pbase holds kc K-chunk slabs [kc][8][d_model]
   int l2keep;                    // not the group's last launch of this layer: keep W_down in L2 (evict_last)
   int xtma;                      // tensor-core-base kernel: stage the x rows with bulk copies (TMA)
+  int early_delta;               // tensor-core-base kernel: first ΔW batch requested before the PDL wait
   // TMA + tcgen05 READ (read_decode_tc.cu): tensor-map extents and its partial-sum workspace
   int L, layer;
   long long n_slot_layers;       // pool slots × L (third extent of the slot tensor map)
@@ -194,6 +195,7 @@ cudaError_t launch_write_rule1(int dtype, const WriteParams &p, cudaStream_t s);
 // bf16, tcgen05: every layer in one launch; cp != nullptr fuses the group commit (last CTA, `arrive`)
 cudaError_t launch_write_tc(const WriteParams &p, const CommitParams *cp, int *arrive, cudaStream_t s);
 bool write_tc_supported(int d_model, int d_ff, int C, int n_layers);
+bool write_tc_triggers_early();   // TTT_WRITE_EARLY_DEP: the WRITE (+ fused commit) triggers dependents at entry
 cudaError_t launch_commit(const CommitParams &p, cudaStream_t s);
 cudaError_t launch_copy(void *dst, const void *src, size_t bytes, cudaStream_t s);
 cudaError_t launch_set_state(int *sel, unsigned long long *version, int *mfail, int idx, int sel_v,

@@ -433,7 +433,20 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_xbar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // r2: a warp whose first task is a ΔW row also requests its first batch before the wait. The
+  // active-slot table and the slot bytes are written only by commit / WRITE / control kernels,
+  // none of which triggers its dependents early (p.early_delta is cleared when the WRITE's early
+  // trigger is switched on), so they completed before this grid was launched.
+  const bool pre_delta = p.early_delta && !early && t < n_tasks;
+  const uint4 *row = nullptr;
   if (early) load_base(cur, t, 0);
+  else if (pre_delta) {
+    const int td = t - n_base, m = td / dm, o = p.owner_idx[m];
+    row = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.slots) +
+                                          (2LL * o + p.sel[o]) * p.slot_elems + p.layer_off) +
+          (size_t)(td - m * dm) * nvec;
+    load_delta(cur, row, lane);
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (tid <= n) {
     if (tid == 0) {
@@ -457,9 +470,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
     }
   }
   __syncthreads();
-  const uint4 *row = nullptr;
   int v = lane;
-  if (!early && t < n_tasks) {
+  if (!early && t < n_tasks && !pre_delta) {
     const int td = t - n_base, m = td / dm;
     row = s_row0[m + 1] + (size_t)(td - m * dm) * nvec;
     load_delta(cur, row, v);
@@ -750,10 +762,12 @@ cudaError_t launch_mma(const ReadParams &p, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   static const int xtma = getenv("TTT_READ_XTMA") ? atoi(getenv("TTT_READ_XTMA")) : 1;
+  static const int early_delta = getenv("TTT_READ_EARLY_DELTA") ? atoi(getenv("TTT_READ_EARLY_DELTA")) : 1;
   ReadParams q = p;
   q.order = order;
   q.dyn = order == 1 ? dyn : 0;
   q.xtma = xtma;
+  q.early_delta = early_delta && !write_tc_triggers_early();
   cudaError_t e = pre1 ? cudaLaunchKernelEx(&cfg, read_decode_mma_kernel<FUSE, L2H, true>, q)
                        : cudaLaunchKernelEx(&cfg, read_decode_mma_kernel<FUSE, L2H, false>, q);
   count_launch();

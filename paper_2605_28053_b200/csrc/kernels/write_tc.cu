@@ -462,8 +462,7 @@ cudaError_t launch_write_tc(const WriteParams &wp, const CommitParams *cp, int *
   p.mfail = wp.mfail;
   p.arrive = arrive;
   p.fuse_commit = cp != nullptr;
-  static const int early_dep = getenv("TTT_WRITE_EARLY_DEP") ? atoi(getenv("TTT_WRITE_EARLY_DEP")) : 0;
-  p.early_dep = early_dep;
+  p.early_dep = write_tc_triggers_early() ? 1 : 0;
   for (int b = 0; b < wp.n; ++b) p.owner_idx[b] = wp.owner_idx[b];
   if (cp) p.cp = *cp;
   const int tiles = wp.n * (wp.d_model / BM) * (wp.d_ff / k.BN);   // per layer (grid = min(SMs, tiles))
@@ -476,6 +475,11 @@ cudaError_t launch_write_tc(const WriteParams &wp, const CommitParams *cp, int *
   }
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+bool write_tc_triggers_early() {
+  static const int early_dep = getenv("TTT_WRITE_EARLY_DEP") ? atoi(getenv("TTT_WRITE_EARLY_DEP")) : 0;
+  return early_dep != 0;
 }
 
 }  // namespace ttt
