@@ -46,10 +46,14 @@ __global__ void __launch_bounds__(512) copy_kernel(uint4 *__restrict__ dst, cons
     for (int k = 0; k < U; ++k) __stcs(dst + i + k * stride, v[k]);
   }
   for (; i < n16; i += stride) dst[i] = src[i];
+  // the decode READ may request its first ΔW batch before its PDL wait (p.early_delta): slot
+  // bytes this copy wrote (rollback from the checkpoint pool, fork) must be visible at exit
+  __threadfence();
 }
 
 __global__ void copy_tail_bytes(unsigned char *dst, const unsigned char *src, size_t n) {
   for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  __threadfence();
 }
 
 __global__ void member_upload_kernel(const __grid_constant__ MemberTable t, int n, int *dst) {
@@ -64,6 +68,7 @@ __global__ void set_state_kernel(int *sel, unsigned long long *version, int *mfa
   sel[idx] = s;
   version[idx] = v;
   mfail[idx] = 0;
+  __threadfence();                               // visible at exit (see copy_kernel)
 }
 
 }  // namespace
