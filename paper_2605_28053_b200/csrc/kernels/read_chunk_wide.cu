@@ -12,8 +12,8 @@
 // ablation without ΔW: ingress -35 %, time -23 %; multicast cut LTS reads but not SM ingress).
 // Here a CTA owns a wider tile (up to 512 accumulator columns of TMEM) and 1/KS of K, and may
 // hold MPC = 2 members that share each W_down box:
-//   * ingress per CTA = (K/KS)·2·(MPC·128 + (1+MPC)·w) bytes; at 8 members the planner picks
-//     MPC = 2, w ≈ 213, KS = 3 (144 CTAs): 6.0 MB per CTA instead of 8.1 MB;
+//   * ingress per CTA = (K/KS)·2·(MPC·128 + (1+MPC)·w) bytes (8 members: 6.4–7.0 MB per CTA
+//     instead of 8.1 MB, e.g. MPC = 2, w ≈ 213, KS = 3 or MPC = 1, w = 288, KS = 2);
 //   * split-K partials are combined in a fixed order (deterministic): CTA ks owns 1/KS of the
 //     tile's 16-column chunks, writes the other chunks' fp32 partials to a workspace slab, and
 //     after the tile's ticket shows all KS slabs, bulk-copies the other CTAs' partials of its own
@@ -21,6 +21,11 @@
 //   * ring: K blocks of 32 (64-byte swizzle) so 3 stages of ~60 KB fit.
 // Every CTA of the grid is resident at once (grid ≤ SM count, one CTA per SM, cooperative
 // launch), which the ticket wait needs.
+//
+// Measured r2 (parity-green, NOT the default — TTT_CHUNK_WIDE=1 selects it): at 8 members
+// 125–163 µs per layer vs 101.5 µs for the narrow kernel (K blocks of 16 / 32 / 64 elements);
+// ncu: fewer L2 -> SM bytes but fewer bytes in flight per SM, and 32-byte rows saturate the
+// SM -> L2 request path (DESIGN §5 f2, profiles/r2/read_chunk_wide_ncu.txt).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
