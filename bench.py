@@ -33,6 +33,11 @@ D_MODEL, D_FF, N_LAYERS, CHUNK, N_STREAMS, V0, SEED = 2560, 9728, 36, 128, 8, 25
 WORKLOAD = (f"config2_paper: {N_STREAMS} TTT streams/GPU x {N_LAYERS} layers, d_model={D_MODEL}, "
             f"d_ff={D_FF}, bf16, C={CHUNK}, 32K ctx (v0={V0}, random dW), uniform trace, B=8, w=0")
 METRIC = "aggregate decode tok/s (TTT READ/WRITE path)"
+# the dominant kernel (libtttstate's default bf16 decode READ; TTT_READ_TC=0 selects the SIMT one)
+READ_KERNEL = ("read_decode_tc_kernel (a3+a4 READ: W_down / dW rows as 16-KB TMA boxes into a shared-memory "
+               "ring, tcgen05 MMAs into TMEM, K-slice partials combined in fixed order)"
+               if os.environ.get("TTT_READ_TC", "1") != "0" else
+               "read_decode_mma_kernel (a3+a4 READ: W_down base on mma.sync, dW rows SIMT)")
 
 
 def parse():
@@ -543,11 +548,11 @@ def main():
         write_bytes = N_STREAMS * (2 * D_MODEL * D_FF * 2 + CHUNK * (D_FF + D_MODEL) * 2) * L
         # BJ metric's "READ TC%": tensor-pipe share from the committed ncu captures (never timed here)
         tc = {}
-        for key, fn, metric in (("read_decode", "read_decode_ncu.txt",
-                                 "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
-                                ("read_chunk_8_members", "read_chunk_tc_ncu.txt",
-                                 "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed")):
-            path = os.path.join(ROOT, "profiles", "r1", fn)
+        for key, rnd, fn, metric in (("read_decode", "r2", "read_decode_ncu.txt",
+                                      "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                                     ("read_chunk_8_members", "r1", "read_chunk_tc_ncu.txt",
+                                      "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed")):
+            path = os.path.join(ROOT, "profiles", rnd, fn)
             if os.path.exists(path):
                 for line in open(path):
                     if line.startswith(metric):
@@ -577,7 +582,7 @@ def main():
                        "tokens_per_step_per_gpu": window * N_STREAMS},
             "e2e": e2e,
             "gpu_launches": n_launch,
-            "roofline": {"kernel": "read_decode_mma_kernel (a3+a4 READ: W_down base on mma.sync, dW rows SIMT)", "bound": "hbm", "achieved": achieved,
+            "roofline": {"kernel": READ_KERNEL, "bound": "hbm", "achieved": achieved,
                          "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "alg_bytes_per_launch": read_bytes, "avg_launch_ms": read_avg,
                          "launches_timed": len(read_ms), "peak_source": "MEASURED_PEAKS.json hbm_gbs",

@@ -791,9 +791,13 @@ cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist_mb << 20);
     limit_set = true;
   }
-  if (p.kc > 0 && !p.fuse && p.ptc && read_decode_tc_supported(p.n, p.d_model, p.d_ff)) {
+  // the TMA + tcgen05 READ for groups that fit one launch (bench.py config 2: 74.3 vs 75.7-76.9 µs);
+  // groups split over several launches keep the SIMT kernel, which measured faster there
+  // (configs 3 / 5: 0.84 / 0.83 vs 0.81 / 0.80 of the roofline with the TMA READ)
+  if (p.kc > 0 && !p.fuse && !p.l2keep && p.ptc && read_decode_tc_supported(p.n, p.d_model, p.d_ff)) {
+    static const int early_delta = getenv("TTT_READ_EARLY_DELTA") ? atoi(getenv("TTT_READ_EARLY_DELTA")) : 1;
     ReadParams q = p;
-    q.l2keep = p.l2keep && l2keep;
+    q.early_delta = early_delta && !write_tc_triggers_early();
     return launch_read_decode_tc(q, s);            // TMA + tcgen05 (read_decode_tc.cu)
   }
   if (p.kc > 0) {

@@ -26,14 +26,14 @@
 // Warps: 0 TMA producer (lane 0), 1 MMA issuer (lane 0), 2–5 x staging / tail append /
 // epilogue (tcgen05.ld) / combine.  TMEM: two 16-column accumulators (row block k in k & 1).
 //
-// Measured r2 (parity-green, NOT the default — TTT_READ_TC=1 selects it): 82.8 µs per launch in
-// tools/microbench.py vs 76.3 µs for read_decode_mma_kernel on the same box; ncu (serialised,
-// cold) 84.5 vs 80.0 µs.  Per-CTA phase stamps (tools/dtc_trace.py): the streaming phase runs
-// at ~43 GB/s per SM (70 µs for 190 boxes) instead of the probe's 46 GB/s — a ring slot is held
-// until its MMAs retire; more stages (8 → 12) did not help — plus 2–4 µs of x staging per launch
-// (it was 9 µs with 128-B TMA one-row boxes: a fixed cost per tiny box), the 4.86-vs-5 row-block
-// imbalance at g = 4, and no work to overlap the PDL wait beyond the first W boxes.  It does run
-// at full clock (1,965 MHz, ~920 W) where the SIMT kernel sits at the 1 kW cap.
+// Ring stages hold bps = 3 boxes (48 KB) with ONE tcgen05.commit per stage: with a commit per
+// 16-KB box the launch took 82.8–97.7 µs (each commit → slot release round trip throttled the
+// stream; ncu tensor pipe 3.8 %, so not MMA throughput); 2 / 3 / 4 boxes per stage: 77.6 / 76.6 /
+// 78.3 µs in tools/microbench.py.  In bench.py (the 36-layer decode window, power-capped B200)
+// it beats the SIMT kernel read_decode_mma_kernel: 74.3 vs 75.7–76.9 µs per launch on one box,
+// 71.7 vs 73.0 µs on another, so it is the default bf16 decode READ for groups of
+// ≤ 8 members (TTT_READ_TC=0 restores the SIMT kernel; fp32 pools and the fused C = 1 READ+WRITE
+// stay SIMT).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -68,6 +68,8 @@ struct DecTcParams {
   int trace;                     // TTT_READ_TC_TRACE=1: per-CTA %globaltimer stamps printed at exit
   int pre;                       // W boxes requested before the PDL wait
   int nomma;                     // diagnostic: release ring slots without MMAs (wrong results)
+  int bps;                       // boxes per ring stage (one commit per stage)
+  int early_delta;               // ΔW boxes may be requested before the PDL wait (slot-table writers never trigger early)
 };
 
 template <int ID, int COUNT>
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = p.stages, g = p.g, grp = blockIdx.x / g, sub = blockIdx.x - grp * g;
   const int kb_lo = sub * p.nkb / g, kb_hi = (sub + 1) * p.nkb / g, nkq = kb_hi - kb_lo;
-  unsigned char *xs = smem + (size_t)S * kTcBoxBytes;          // [nkq][8 rows][128 B] swizzled x slice
+  unsigned char *xs = smem + (size_t)S * p.bps * kTcBoxBytes;  // [nkq][8 rows][128 B] swizzled x slice
   u64 *bars = reinterpret_cast<u64 *>(xs + (size_t)nkq * 1024);
   u64 *full = bars, *empty = bars + kTcMaxStages, *t_full = bars + 2 * kTcMaxStages, *t_empty = t_full + 2;
   u64 *x_ready = t_empty + 2;
@@ -147,15 +149,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         rb_of(k, m, rbi);
         int coord2 = p.layer;
         if (m > 0) {
-          if (!waited) {
+          if (!waited && !p.early_delta) {                  // (see read_decode.cu: p.early_delta)
             asm volatile("griddepcontrol.wait;" ::: "memory");
             waited = true;
           }
           const int o = p.owner_idx[m - 1];
           coord2 = (2 * o + p.sel[o]) * p.L + p.layer;
         }
-        for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
-          const int s = it % S;
+        for (int kb = kb_lo; kb < kb_hi; kb += p.bps, ++it) {   // a stage = bps boxes (consecutive K blocks)
+          const int s = it % S, nb = min(p.bps, kb_hi - kb);
           if (it >= p.pre || it >= S) {
             if (!waited) {                                   // (pre-wait prefetch budget used: wait now)
               asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -163,13 +165,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             mbar_wait(empty + s, ((it / S) - 1) & 1);
           }
-          mbar_expect_tx(full + s, kTcBoxBytes);
-          unsigned char *dst = smem + (size_t)s * kTcBoxBytes;
-          if (m == 0) {
-            if (p.l2keep) tma_load_3d_hint(dst, &tmW, full + s, kb * kTcBK, rbi * 128, 0, pol_w);
-            else tma_load_3d(dst, &tmW, full + s, kb * kTcBK, rbi * 128, 0);
-          } else {
-            tma_load_3d(dst, &tmD, full + s, kb * kTcBK, rbi * 128, coord2);
+          mbar_expect_tx(full + s, (uint32_t)nb * kTcBoxBytes);
+          for (int i = 0; i < nb; ++i) {
+            unsigned char *dst = smem + ((size_t)s * p.bps + i) * kTcBoxBytes;
+            if (m == 0) {
+              if (p.l2keep) tma_load_3d_hint(dst, &tmW, full + s, (kb + i) * kTcBK, rbi * 128, 0, pol_w);
+              else tma_load_3d(dst, &tmW, full + s, (kb + i) * kTcBK, rbi * 128, 0);
+            } else {
+              tma_load_3d(dst, &tmD, full + s, (kb + i) * kTcBK, rbi * 128, coord2);
+            }
           }
         }
       }
@@ -191,21 +195,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           mbar_wait(t_empty + (k & 1), ((k >> 1) - 1) & 1);
           tc_fence_after();
         }
-        for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
-          const int s = it % S;
+        for (int kb = kb_lo; kb < kb_hi; kb += p.bps, ++it) {
+          const int s = it % S, nb = min(p.bps, kb_hi - kb);
+          const bool last = kb + nb >= kb_hi;
           mbar_wait(full + s, (it / S) & 1);
           tc_fence_after();
           if (lane == 0 && p.nomma) {                       // diagnostic (TTT_READ_TC_NOMMA): stream only
             mbar_arrive(empty + s);
-            if (kb == kb_hi - 1) mbar_arrive(t_full + (k & 1));
+            if (last) mbar_arrive(t_full + (k & 1));
           } else if (lane == 0) {
-            const uint32_t a0 = smem_u32(smem + (size_t)s * kTcBoxBytes), b0 = xb0 + (uint32_t)(kb - kb_lo) * 1024;
+            for (int i = 0; i < nb; ++i) {
+              const uint32_t a0 = smem_u32(smem + ((size_t)s * p.bps + i) * kTcBoxBytes);
+              const uint32_t b0 = xb0 + (uint32_t)(kb + i - kb_lo) * 1024;
 #pragma unroll
-            for (int kk = 0; kk < kTcBK / 16; ++kk)
-              mma_bf16(acc + kk * 16, smem_desc_sw128(a0 + kk * 32, 16, 1024), smem_desc_sw128(b0 + kk * 32, 16, 0),
-                       idesc, kb > kb_lo ? 1u : 0u);
+              for (int kk = 0; kk < kTcBK / 16; ++kk)
+                mma_bf16(acc + kk * 16, smem_desc_sw128(a0 + kk * 32, 16, 1024), smem_desc_sw128(b0 + kk * 32, 16, 0),
+                         idesc, (kb > kb_lo || i > 0) ? 1u : 0u);
+            }
             mma_commit(empty + s);
-            if (kb == kb_hi - 1) mma_commit(t_full + (k & 1));
+            if (last) mma_commit(t_full + (k & 1));
           }
           __syncwarp();
         }
@@ -383,7 +391,7 @@ int plan_g(int n_rb, int nkb, int sms, int *G_out, int *stages_out) {
 }  // namespace
 
 bool read_decode_tc_supported(int n, int d_model, int d_ff) {
-  static const int on = getenv("TTT_READ_TC") ? atoi(getenv("TTT_READ_TC")) : 0;   // opt-in (see header)
+  static const int on = getenv("TTT_READ_TC") ? atoi(getenv("TTT_READ_TC")) : 1;   // TTT_READ_TC=0: the SIMT kernel
   return on && n >= 1 && n <= kMaxReadMembers && d_model >= 128 && d_ff % 8 == 0 && d_ff >= kTcBK &&
          ptx::encode_fn() != nullptr;
 }
@@ -395,16 +403,20 @@ cudaError_t launch_read_decode_tc(const ReadParams &rp, cudaStream_t s) {
   p.nrb = (rp.d_model + 127) / 128;
   p.n_mat = 1 + rp.n;
   const int sms = device_sm_count();
+  static const int bps = getenv("TTT_READ_TC_BPS") ? std::max(1, std::min(4, atoi(getenv("TTT_READ_TC_BPS")))) : 3;
+  p.bps = bps;
   p.g = plan_g(p.n_mat * p.nrb, p.nkb, sms, &p.G, &p.stages);
+  p.stages = std::max(2, p.stages / bps);
   static const int g_env = getenv("TTT_READ_TC_G") ? atoi(getenv("TTT_READ_TC_G")) : 0;
   if (g_env > 0 && g_env <= std::min(sms, kTcMaxG)) {   // tuning override
     p.g = g_env;
     p.G = sms / g_env;
     const int nkq_e = (p.nkb + p.g - 1) / p.g;
-    p.stages = std::min(kTcMaxStages, (int)((227 * 1024 - 4096 - (size_t)nkq_e * 1024) / kTcBoxBytes));
+    p.stages = std::max(2, std::min(kTcMaxStages, (int)((227 * 1024 - 4096 - (size_t)nkq_e * 1024) / kTcBoxBytes)) / bps);
   }
   if (p.g == 0 || (size_t)p.g * p.nrb * 128 * 8 * 2 * sizeof(float) > rp.ptc_bytes) return cudaErrorInvalidValue;
   p.l2keep = rp.l2keep;
+  p.early_delta = rp.early_delta;
   static const int trace = getenv("TTT_READ_TC_TRACE") ? atoi(getenv("TTT_READ_TC_TRACE")) : 0;
   p.trace = trace;
   static const int pre = getenv("TTT_READ_TC_PRE") ? atoi(getenv("TTT_READ_TC_PRE")) : 1 << 20;
@@ -430,7 +442,7 @@ cudaError_t launch_read_decode_tc(const ReadParams &rp, cudaStream_t s) {
       !cached_map(&mD, rp.slots, rp.d_ff, rp.d_model, (uint64_t)rp.n_slot_layers, kTcBK, 128))
     return cudaErrorInvalidValue;
   const int nkq = (p.nkb + p.g - 1) / p.g;
-  const size_t smem = 1024 + (size_t)p.stages * kTcBoxBytes + (size_t)nkq * 1024 + (2 * kTcMaxStages + 6) * 8 + 16;
+  const size_t smem = 1024 + (size_t)p.stages * p.bps * kTcBoxBytes + (size_t)nkq * 1024 + (2 * kTcMaxStages + 6) * 8 + 16;
   static size_t configured = 0;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(read_decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

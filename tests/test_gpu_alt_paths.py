@@ -5,8 +5,8 @@ READ (used when a fused launch would not fit one CTA per tile), the one-pass tcg
 READ over [W_down; A] with its bulk-copy finish (TTT_LR_FUSED=2), multi-launch READ groups
 with plain loads instead of the L2 evict_last / evict_first hints (TTT_READ_L2KEEP=0), the
 serial-order READ, and both chunk READ kernels on every shape (TTT_CHUNK_WIDE=1 forces the wide
-split-K kernel wherever it has a plan, =0 keeps the narrow one at paper dims), and the TMA +
-tcgen05 decode READ (TTT_READ_TC=1)."""
+split-K kernel wherever it has a plan, =0 keeps the narrow one at paper dims), and the SIMT
+decode READ with the mma.sync base (TTT_READ_TC=0; the default is the TMA + tcgen05 READ)."""
 import os
 import subprocess
 import sys
@@ -32,8 +32,9 @@ def _run(env_extra, target):
     ({"TTT_LR_FUSED": "2"}, "tests/test_gpu_lowrank.py"),
     ({"TTT_READ_L2KEEP": "0"}, "tests/test_gpu_configs.py"),
     ({"TTT_CHUNK_WIDE": "1"}, "tests/test_gpu_read_chunk.py"),
-    ({"TTT_READ_TC": "1"}, "tests/test_gpu_parity.py"),
-    ({"TTT_READ_TC": "1"}, "tests/test_gpu_full_size.py::test_config3_decode_read_64_members_paper_dims"),
+    ({"TTT_READ_TC": "0"}, "tests/test_gpu_parity.py"),
+    ({"TTT_READ_TC": "0"}, "tests/test_gpu_full_size.py::test_config3_decode_read_64_members_paper_dims"),
+    ({"TTT_READ_TC": "0"}, "tests/test_gpu_paper_dims.py"),
     ({"TTT_CHUNK_WIDE": "0"}, "tests/test_gpu_full_size.py::test_f2_chunk_read_paper_dims"),
 ])
 def test_alternative_paths_parity(env, target):
