@@ -798,7 +798,9 @@ cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s) {
     static const int early_delta = getenv("TTT_READ_EARLY_DELTA") ? atoi(getenv("TTT_READ_EARLY_DELTA")) : 1;
     ReadParams q = p;
     q.early_delta = early_delta && !write_tc_triggers_early();
-    return launch_read_decode_tc(q, s);            // TMA + tcgen05 (read_decode_tc.cu)
+    const cudaError_t e = launch_read_decode_tc(q, s);   // TMA + tcgen05 (read_decode_tc.cu)
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();                            // no plan for this shape: the SIMT kernel below
   }
   if (p.kc > 0) {
     if (p.l2keep && l2keep) return p.fuse ? launch_mma<true, true>(p, s) : launch_mma<false, true>(p, s);

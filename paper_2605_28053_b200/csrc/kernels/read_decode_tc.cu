@@ -414,7 +414,8 @@ cudaError_t launch_read_decode_tc(const ReadParams &rp, cudaStream_t s) {
     const int nkq_e = (p.nkb + p.g - 1) / p.g;
     p.stages = std::max(2, std::min(kTcMaxStages, (int)((227 * 1024 - 4096 - (size_t)nkq_e * 1024) / kTcBoxBytes)) / bps);
   }
-  if (p.g == 0 || (size_t)p.g * p.nrb * 128 * 8 * 2 * sizeof(float) > rp.ptc_bytes) return cudaErrorInvalidValue;
+  // no plan for this shape: cudaErrorNotSupported, and launch_read_decode runs the SIMT kernel
+  if (p.g == 0 || (size_t)p.g * p.nrb * 128 * 8 * 2 * sizeof(float) > rp.ptc_bytes) return cudaErrorNotSupported;
   p.l2keep = rp.l2keep;
   p.early_delta = rp.early_delta;
   static const int trace = getenv("TTT_READ_TC_TRACE") ? atoi(getenv("TTT_READ_TC_TRACE")) : 0;
