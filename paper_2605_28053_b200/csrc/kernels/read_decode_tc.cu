@@ -12,28 +12,32 @@
 // for the 1024-thread register-batch kernel, whose warps run out of rows at different times.
 // So: every weight byte arrives as a 128-row × 64-column box (16 KB, 128-byte swizzle) and the
 // tensor core does the products — the weight rows are the MMA's A operand (M = 128) and the
-// members' x rows its B operand (N = 16: 8 member rows + 8 zero rows), accumulating
-// D[128 rows × 16] in TMEM.  For a ΔW_b box only column b of D is wanted (15/16 of that MMA is
-// thrown away — a few % of the tensor pipe, irrelevant next to the HBM stream).
+// members' x rows its B operand (N = 16: the 8 member rows, rows 8..15 aliased onto them by a
+// zero stride), accumulating D[128 rows × 16] in TMEM.  For a ΔW_b box only column b of D is
+// wanted (15/16 of that MMA is thrown away — a few % of the tensor pipe, irrelevant next to the
+// HBM stream).
 //
-// Work split: the 9 matrices (W_down, ΔW_0 … ΔW_7) × ⌈d_model/128⌉ row blocks are dealt to G
-// groups of g CTAs; CTA `sub` of a group streams K blocks [sub·nkb/g, (sub+1)·nkb/g) of each of
-// its group's row blocks, so its slice of the x rows (8 rows × its K range) is staged in shared
-// memory once.  g is chosen to balance K blocks per CTA (g = 4 at paper dims: 37 groups, 38 K
-// blocks of 64 per row block).  Each (row block, K slice) partial goes to a workspace slab; the
-// last of the (1+n)·g arrivals for an output row block (per-row-block ticket) sums, in a fixed
-// order, Σ_slices W-partial[b] + Σ_slices ΔW_b-partial (+ resid) → bf16 y (deterministic).
-// Warps: 0 TMA producer (lane 0), 1 MMA issuer (lane 0), 2–5 x staging / tail append /
-// epilogue (tcgen05.ld) / combine.  TMEM: two 16-column accumulators (row block k in k & 1).
+// Work split: the 1+n matrices (W_down, ΔW_0 … ΔW_{n-1}) × ⌈d_model/128⌉ row blocks are dealt
+// round-robin to G groups of g CTAs; CTA `sub` of a group streams K blocks [sub·nkb/g,
+// (sub+1)·nkb/g) of each of its group's row blocks, so its slice of the x rows is staged in shared
+// memory once.  plan_g picks g to minimise the busiest CTA's boxes, then the smallest x slice
+// (most ring stages): at paper dims g = 8, G = 18 (144 CTAs, 10 row blocks × 19 K blocks each).
+// Each (row block, K slice) partial goes to a workspace slab; the last of the (1+n)·g arrivals
+// for an output row block (per-row-block ticket) sums, in a fixed order, Σ_slices W-partial[b] +
+// Σ_slices ΔW_b-partial (+ resid) → bf16 y (deterministic).  Warps: 0 TMA producer (lane 0),
+// 1 MMA issuer (lane 0), 2–5 x staging / tail append / epilogue (tcgen05.ld) / combine.  TMEM:
+// per row block 4 accumulators of 16 columns (one per K = 16 step of a box, summed in order in
+// the epilogue), double-buffered (row block k in k & 1).
 //
 // Ring stages hold bps = 3 boxes (48 KB) with ONE tcgen05.commit per stage: with a commit per
 // 16-KB box the launch took 82.8–97.7 µs (each commit → slot release round trip throttled the
 // stream; ncu tensor pipe 3.8 %, so not MMA throughput); 2 / 3 / 4 boxes per stage: 77.6 / 76.6 /
-// 78.3 µs in tools/microbench.py.  In bench.py (the 36-layer decode window, power-capped B200)
-// it beats the SIMT kernel read_decode_mma_kernel: 74.3 vs 75.7–76.9 µs per launch on one box,
-// 71.7 vs 73.0 µs on another, so it is the default bf16 decode READ for groups of
-// ≤ 8 members (TTT_READ_TC=0 restores the SIMT kernel; fp32 pools and the fused C = 1 READ+WRITE
-// stay SIMT).
+// 78.3 µs in tools/microbench.py.  In bench.py (the 36-layer decode window) it beats the SIMT
+// kernel read_decode_mma_kernel: 74.0–74.3 vs 74.7–76.9 µs per launch on power-capped boxes,
+// 73.9 µs = 0.929 of HBM in the final run, so it is the default bf16 decode READ for
+// groups that fit one launch (≤ 8 members).  Groups split over several launches (configs 3 / 5)
+// keep the SIMT kernel, measured faster there; TTT_READ_TC=0 restores it everywhere; fp32 pools
+// and the fused C = 1 READ+WRITE always use it.
 #include <algorithm>
 #include <mutex>
 #include <cstdio>
