@@ -253,6 +253,22 @@ def _random_shapes(n, seed):
     return out
 
 
+def _tc_read_shapes(n, seed):
+    """bf16 shapes the TMA + tcgen05 decode READ serves (d_model >= 128, d_ff >= 64, ≤ 8 members):
+    row blocks and 64-wide K boxes both ragged (TMA out-of-bounds fill), 1..8 members."""
+    g = np.random.default_rng(seed)
+    return [(int(g.integers(32, 180)) * 4, int(g.integers(8, 150)) * 8, int(g.integers(1, 9)), int(g.integers(1 << 30)))
+            for _ in range(n)]
+
+
+@pytest.mark.parametrize("d_model,d_ff,streams,seed", _tc_read_shapes(8, 77))
+def test_tc_read_ragged_shapes_parity(d_model, d_ff, streams, seed):
+    tr = T.uniform_small(n_streams=streams, n_layers=2, d_model=d_model, d_ff=d_ff, chunk=8, n_steps=18, dtype="bf16",
+                         delta0="rng", v0=1, seed=seed % 1000)
+    ref, src, log, eng = _run(tr)
+    _compare(tr, ref, src, log, eng)
+
+
 @pytest.mark.parametrize("dtype,d_model,d_ff,streams,chunk,seed", _random_shapes(6, 2026))
 def test_random_shapes_parity(dtype, d_model, d_ff, streams, chunk, seed):
     """Seeded random shapes: ragged row blocks / K chunks / vector tails, 1..12 members
