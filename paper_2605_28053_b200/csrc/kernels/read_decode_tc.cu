@@ -55,6 +55,10 @@ constexpr int kTcThreads = 192;
 constexpr int kTcBK = 64;                          // K elements per box (128 B rows)
 constexpr int kTcBoxBytes = 128 * kTcBK * 2;       // 16 KB
 constexpr int kTcMaxStages = 12;
+#ifndef TTT_TC_COMBINE_BATCH
+#define TTT_TC_COMBINE_BATCH 8
+#endif
+constexpr int kCombineBatch = TTT_TC_COMBINE_BATCH;   // K slices whose partials one combine round trip loads
 
 struct DecTcParams {
   int n, d_model, d_ff, L, layer;
@@ -318,14 +322,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int i = rbi * 128 + et;
         if (i < dm) {
           // y_b = Σ_slices W-partial[b] + Σ_slices ΔW_b-partial, slices ascending; the loads of
-          // four slices are issued together (one L2 round trip per four slices)
+          // kCombineBatch slices are issued together (one L2 round trip at the g = 8 plan)
           float w[8], d[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) w[e] = d[e] = 0.f;
-          for (int s0 = 0; s0 < g; s0 += 4) {
-            float4 lw[4][2], ld[4][2];
+          for (int s0 = 0; s0 < g; s0 += kCombineBatch) {
+            float4 lw[kCombineBatch][2], ld[kCombineBatch][2];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kCombineBatch; ++u) {
               const bool ok = s0 + u < g;
               const float4 *pw = reinterpret_cast<const float4 *>(p.Pw + ((size_t)(s0 + u) * rows_pad + i) * 8);
               const float4 *pd = reinterpret_cast<const float4 *>(p.Pd + ((size_t)(s0 + u) * rows_pad + i) * 8);
@@ -336,7 +340,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               ld[u][1] = ok ? __ldcg(pd + 1) : z;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kCombineBatch; ++u) {
               if (s0 + u >= g) break;
               w[0] += lw[u][0].x; w[1] += lw[u][0].y; w[2] += lw[u][0].z; w[3] += lw[u][0].w;
               w[4] += lw[u][1].x; w[5] += lw[u][1].y; w[6] += lw[u][1].z; w[7] += lw[u][1].w;
