@@ -38,6 +38,10 @@
 // groups that fit one launch (≤ 8 members).  Groups split over several launches (configs 3 / 5)
 // keep the SIMT kernel, measured faster there; TTT_READ_TC=0 restores it everywhere; fp32 pools
 // and the fused C = 1 READ+WRITE always use it.
+//
+// TTT_READ_TC_HYB = h (opt-in, measured not kept): warps 6–9 stream the CTA's last h ΔW row blocks
+// through registers next to the TMA ring (more bytes in flight per SM).  h = 1 / 2 / 3: 74.8 / 76.6 /
+// 87.4 µs per launch vs 74.2–75.4 default on the same box — the launch is DRAM-rate bound here.
 #include <algorithm>
 #include <mutex>
 #include <cstdio>
@@ -52,6 +56,9 @@ namespace {
 using namespace ptx;
 
 constexpr int kTcThreads = 192;
+constexpr int kHybWarps = 4;                       // TTT_READ_TC_HYB: register-streaming ΔW warps (6..9)
+constexpr int kHybRows = 4;                        // rows per warp batch (all their loads in flight)
+constexpr int kHybLd = 5;                          // 16-B loads per lane per row (K slice ≤ 5·32·8 elements)
 constexpr int kTcBK = 64;                          // K elements per box (128 B rows)
 constexpr int kTcBoxBytes = 128 * kTcBK * 2;       // 16 KB
 constexpr int kTcMaxStages = 12;
@@ -79,6 +86,8 @@ struct DecTcParams {
   int nomma;                     // diagnostic: release ring slots without MMAs (wrong results)
   int bps;                       // boxes per ring stage (one commit per stage)
   int early_delta;               // ΔW boxes may be requested before the PDL wait (slot-table writers never trigger early)
+  int hyb;                       // the CTA's last `hyb` ΔW row blocks go to register-streaming warps, not TMA
+  const __nv_bfloat16 *slots;    // slot array (the tmD tensor: [n_slot_layers][d_model][d_ff])
 };
 
 template <int ID, int COUNT>
@@ -93,7 +102,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreads + 32 * kHybWarps, 1)
     read_decode_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmD,
                           const DecTcParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -105,7 +114,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   u64 *full = bars, *empty = bars + kTcMaxStages, *t_full = bars + 2 * kTcMaxStages, *t_empty = t_full + 2;
   u64 *x_ready = t_empty + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(x_ready + 1);
-  __shared__ int s_last;
+  __shared__ int s_last, s_last_h;
   __shared__ unsigned long long ts[7];
   auto stamp = [&](int i) {
     if (p.trace) {
@@ -123,6 +132,55 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int r = grp + k * p.G;
     m = r / p.nrb;
     rbi = r - m * p.nrb;
+  };
+  // hybrid split: the last h row blocks (ΔW only) are streamed by warps 6.. through registers
+  int h = 0;
+  while (h < p.hyb && h + 1 < my_rbs && (grp + (my_rbs - 1 - h) * p.G) / p.nrb > 0) ++h;
+  const int kt = my_rbs - h;                                     // row blocks through TMA + tcgen05
+
+  // combine output row block rbi (fixed order), by the 128 threads t of the last-arriving group
+  auto combine = [&](const int rbi, const int t) {
+    const int rows_pad = p.nrb * 128, dm = p.d_model, n = p.n;
+    __threadfence();
+    const int i = rbi * 128 + t;
+    if (i < dm) {
+      // y_b = Σ_slices W-partial[b] + Σ_slices ΔW_b-partial, slices ascending; the loads of
+      // kCombineBatch slices are issued together (one L2 round trip at the g = 8 plan)
+      float w[8], d[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) w[e] = d[e] = 0.f;
+      for (int s0 = 0; s0 < g; s0 += kCombineBatch) {
+        float4 lw[kCombineBatch][2], ld[kCombineBatch][2];
+#pragma unroll
+        for (int u = 0; u < kCombineBatch; ++u) {
+          const bool ok = s0 + u < g;
+          const float4 *pw = reinterpret_cast<const float4 *>(p.Pw + ((size_t)(s0 + u) * rows_pad + i) * 8);
+          const float4 *pd = reinterpret_cast<const float4 *>(p.Pd + ((size_t)(s0 + u) * rows_pad + i) * 8);
+          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+          lw[u][0] = ok ? __ldcg(pw) : z;
+          lw[u][1] = ok ? __ldcg(pw + 1) : z;
+          ld[u][0] = ok ? __ldcg(pd) : z;
+          ld[u][1] = ok ? __ldcg(pd + 1) : z;
+        }
+#pragma unroll
+        for (int u = 0; u < kCombineBatch; ++u) {
+          if (s0 + u >= g) break;
+          w[0] += lw[u][0].x; w[1] += lw[u][0].y; w[2] += lw[u][0].z; w[3] += lw[u][0].w;
+          w[4] += lw[u][1].x; w[5] += lw[u][1].y; w[6] += lw[u][1].z; w[7] += lw[u][1].w;
+          d[0] += ld[u][0].x; d[1] += ld[u][0].y; d[2] += ld[u][0].z; d[3] += ld[u][0].w;
+          d[4] += ld[u][1].x; d[5] += ld[u][1].y; d[6] += ld[u][1].z; d[7] += ld[u][1].w;
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        if (b >= n) break;
+        float y = w[b] + d[b];
+        if (p.resid)
+          y += __bfloat162float(static_cast<const __nv_bfloat16 *>(p.resid)[(size_t)p.y_row[b] * dm + i]);
+        static_cast<__nv_bfloat16 *>(p.Y)[(size_t)p.y_row[b] * dm + i] = __float2bfloat16_rn(y);
+      }
+    }
+    if (t == 0) p.tickets[rbi] = 0;                         // self-reset for the next launch
   };
 
   if (threadIdx.x == 0) {
@@ -153,7 +211,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // W_down is never written by any kernel: this group's W boxes may be requested before the
       // PDL wait (ΔW boxes need the slot table, written by commits)
       bool waited = false;
-      for (int k = 0; k < my_rbs; ++k) {
+      for (int k = 0; k < kt; ++k) {
         int m, rbi;
         rb_of(k, m, rbi);
         int coord2 = p.layer;
@@ -198,7 +256,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const uint32_t idesc = idesc_bf16(128, 16, 0, 0);
       const uint32_t xb0 = smem_u32(xs);
       int it = 0;
-      for (int k = 0; k < my_rbs; ++k) {
+      for (int k = 0; k < kt; ++k) {
         const uint32_t acc = tmem + (uint32_t)((k & 1) * 64);   // 4 accumulators of 16 columns (one per K=16 step)
         if (k >= 2) {
           mbar_wait(t_empty + (k & 1), ((k >> 1) - 1) & 1);
@@ -228,7 +286,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
     }
-  } else {                                                  // ---------------- warps 2-5
+  } else if (warp < 6) {                                    // ---------------- warps 2-5
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 64) stamp(5);
     const int q = warp & 3, et = threadIdx.x - 64;
@@ -275,7 +333,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
     const int rows_pad = p.nrb * 128;
-    for (int k = 0; k < my_rbs; ++k) {
+    for (int k = 0; k < kt; ++k) {
       int m, rbi;
       rb_of(k, m, rbi);
       mbar_wait(t_full + (k & 1), (k >> 1) & 1);
@@ -317,49 +375,79 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         s_last = atomicAdd(p.tickets + rbi, 1) == p.n_mat * g - 1;
       }
       named_bar<1, 128>();
-      if (s_last) {                                         // combine output row block rbi (fixed order)
-        __threadfence();
-        const int i = rbi * 128 + et;
-        if (i < dm) {
-          // y_b = Σ_slices W-partial[b] + Σ_slices ΔW_b-partial, slices ascending; the loads of
-          // kCombineBatch slices are issued together (one L2 round trip at the g = 8 plan)
-          float w[8], d[8];
+      if (s_last) combine(rbi, et);                         // output row block rbi (fixed order)
+    }
+  } else if (h > 0) {                                       // ---------------- warps 6..: hybrid ΔW rows
+    // The CTA's last h ΔW row blocks, K slice [kb_lo, kb_hi), streamed through registers (16-B
+    // loads, kHybRows rows × kHybLd loads per lane in flight) next to the TMA ring, so the SM has the
+    // ring's and the registers' bytes in flight at once; products against the swizzled x slice in
+    // shared memory, a fixed-order warp reduction, then the same partial record, ticket and
+    // combine as the tcgen05 epilogue.
+    const int hw = warp - 6, ht = threadIdx.x - kTcThreads;
+    const int rows_pad = p.nrb * 128, dff = p.d_ff, kel0 = kb_lo * kTcBK, klen = min(nkq * kTcBK, dff - kel0);
+    const int nch = klen >> 3;                                // 16-B chunks in the K slice
+    if (!p.early_delta) asm volatile("griddepcontrol.wait;" ::: "memory");
+    bool xwait = true;
+    for (int j = 0; j < h; ++j) {
+      int m, rbi;
+      rb_of(kt + j, m, rbi);
+      const int b = m - 1, o = p.owner_idx[b];
+      const __nv_bfloat16 *base = p.slots + ((size_t)((2 * o + p.sel[o]) * p.L + p.layer) * p.d_model) * dff + kel0;
+      for (int r0 = hw * kHybRows; r0 < 128; r0 += kHybWarps * kHybRows) {
+        uint4 v[kHybRows][kHybLd];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) w[e] = d[e] = 0.f;
-          for (int s0 = 0; s0 < g; s0 += kCombineBatch) {
-            float4 lw[kCombineBatch][2], ld[kCombineBatch][2];
+        for (int rr = 0; rr < kHybRows; ++rr) {
+          const int row = rbi * 128 + r0 + rr;
 #pragma unroll
-            for (int u = 0; u < kCombineBatch; ++u) {
-              const bool ok = s0 + u < g;
-              const float4 *pw = reinterpret_cast<const float4 *>(p.Pw + ((size_t)(s0 + u) * rows_pad + i) * 8);
-              const float4 *pd = reinterpret_cast<const float4 *>(p.Pd + ((size_t)(s0 + u) * rows_pad + i) * 8);
-              const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-              lw[u][0] = ok ? __ldcg(pw) : z;
-              lw[u][1] = ok ? __ldcg(pw + 1) : z;
-              ld[u][0] = ok ? __ldcg(pd) : z;
-              ld[u][1] = ok ? __ldcg(pd + 1) : z;
-            }
-#pragma unroll
-            for (int u = 0; u < kCombineBatch; ++u) {
-              if (s0 + u >= g) break;
-              w[0] += lw[u][0].x; w[1] += lw[u][0].y; w[2] += lw[u][0].z; w[3] += lw[u][0].w;
-              w[4] += lw[u][1].x; w[5] += lw[u][1].y; w[6] += lw[u][1].z; w[7] += lw[u][1].w;
-              d[0] += ld[u][0].x; d[1] += ld[u][0].y; d[2] += ld[u][0].z; d[3] += ld[u][0].w;
-              d[4] += ld[u][1].x; d[5] += ld[u][1].y; d[6] += ld[u][1].z; d[7] += ld[u][1].w;
-            }
-          }
-#pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            if (b >= n) break;
-            float y = w[b] + d[b];
-            if (p.resid)
-              y += __bfloat162float(static_cast<const __nv_bfloat16 *>(p.resid)[(size_t)p.y_row[b] * dm + i]);
-            static_cast<__nv_bfloat16 *>(p.Y)[(size_t)p.y_row[b] * dm + i] = __float2bfloat16_rn(y);
+          for (int u = 0; u < kHybLd; ++u) {
+            const int c = lane + 32 * u;
+            v[rr][u] = make_uint4(0u, 0u, 0u, 0u);
+            if (row < p.d_model && c < nch) v[rr][u] = __ldcs(reinterpret_cast<const uint4 *>(base + (size_t)row * dff) + c);
           }
         }
-        if (et == 0) p.tickets[rbi] = 0;                    // self-reset for the next launch
+        if (xwait) {
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          mbar_wait(x_ready, 0);
+          xwait = false;
+        }
+        float acc[kHybRows];
+#pragma unroll
+        for (int rr = 0; rr < kHybRows; ++rr) acc[rr] = 0.f;
+#pragma unroll
+        for (int u = 0; u < kHybLd; ++u) {
+          const int c = lane + 32 * u;
+          if (c < nch) {
+            const uint4 xv = *reinterpret_cast<const uint4 *>(xs + (size_t)(c >> 3) * 1024 + b * 128 + (((c & 7) ^ b) << 4));
+            const __nv_bfloat162 *x2 = reinterpret_cast<const __nv_bfloat162 *>(&xv);
+#pragma unroll
+            for (int rr = 0; rr < kHybRows; ++rr) {
+              const __nv_bfloat162 *w2 = reinterpret_cast<const __nv_bfloat162 *>(&v[rr][u]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 wf = __bfloat1622float2(w2[e]), xf = __bfloat1622float2(x2[e]);
+                acc[rr] = fmaf(wf.x, xf.x, acc[rr]);
+                acc[rr] = fmaf(wf.y, xf.y, acc[rr]);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < kHybRows; ++rr) {
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], off);
+          const int row = rbi * 128 + r0 + rr;
+          if (lane == 0) __stcg(p.Pd + ((size_t)sub * rows_pad + row) * 8 + b, acc[rr]);
+        }
       }
+      named_bar<2, 32 * kHybWarps>();                       // the row block's partials are stored
+      if (ht == 0) {
+        __threadfence();
+        s_last_h = atomicAdd(p.tickets + rbi, 1) == p.n_mat * g - 1;
+      }
+      named_bar<2, 32 * kHybWarps>();
+      if (s_last_h) combine(rbi, ht);
     }
+    if (xwait) asm volatile("griddepcontrol.wait;" ::: "memory");
   }
   if (threadIdx.x == 64) stamp(3);
   tc_fence_before();
@@ -461,6 +549,9 @@ cudaError_t launch_read_decode_tc(const ReadParams &rp, cudaStream_t s) {
   p.pre = pre;
   static const int nomma = getenv("TTT_READ_TC_NOMMA") ? atoi(getenv("TTT_READ_TC_NOMMA")) : 0;
   p.nomma = nomma;
+  static const int hyb = getenv("TTT_READ_TC_HYB") ? atoi(getenv("TTT_READ_TC_HYB")) : 0;
+  p.hyb = ((p.nkb + p.g - 1) / p.g) * kTcBK <= kHybLd * 32 * 8 ? hyb : 0;   // (K slice within the warps' loads)
+  p.slots = static_cast<const __nv_bfloat16 *>(rp.slots);
   p.sel = rp.sel;
   p.X = rp.X; p.Vt = rp.Vt; p.resid = rp.resid; p.Y = rp.Y;
   p.tailZ = rp.tailZ; p.tailV = rp.tailV;
@@ -499,7 +590,7 @@ cudaError_t launch_read_decode_tc(const ReadParams &rp, cudaStream_t s) {
   static const bool pdl = !getenv("TTT_PDL") || atoi(getenv("TTT_PDL")) != 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(sms);
-  cfg.blockDim = dim3(kTcThreads);
+  cfg.blockDim = dim3(kTcThreads + (p.hyb > 0 ? 32 * kHybWarps : 0));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -6,7 +6,8 @@ READ over [W_down; A] with its bulk-copy finish (TTT_LR_FUSED=2), multi-launch R
 with plain loads instead of the L2 evict_last / evict_first hints (TTT_READ_L2KEEP=0), the
 serial-order READ, and both chunk READ kernels on every shape (TTT_CHUNK_WIDE=1 forces the wide
 split-K kernel wherever it has a plan, =0 keeps the narrow one at paper dims), and the SIMT
-decode READ with the mma.sync base (TTT_READ_TC=0; the default is the TMA + tcgen05 READ)."""
+decode READ with the mma.sync base (TTT_READ_TC=0; the default is the TMA + tcgen05 READ), and
+the TMA + tcgen05 READ with its last ΔW row blocks streamed by register warps (TTT_READ_TC_HYB)."""
 import os
 import subprocess
 import sys
@@ -36,6 +37,8 @@ def _run(env_extra, target):
     ({"TTT_READ_TC": "0"}, "tests/test_gpu_full_size.py::test_config3_decode_read_64_members_paper_dims"),
     ({"TTT_READ_TC": "0"}, "tests/test_gpu_paper_dims.py"),
     ({"TTT_CHUNK_WIDE": "0"}, "tests/test_gpu_full_size.py::test_f2_chunk_read_paper_dims"),
+    ({"TTT_READ_TC_HYB": "2"}, "tests/test_gpu_parity.py"),
+    ({"TTT_READ_TC_HYB": "1"}, "tests/test_gpu_paper_dims.py"),
 ])
 def test_alternative_paths_parity(env, target):
     _run(env, target)
