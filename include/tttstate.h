@@ -262,7 +262,11 @@ ttt_status tttstate_last_commit_seq(ttt_pool *pool, uint64_t *seq_out);
 /* Inputs/outputs of one decode step: the token of owners[i] sits at row rows[i]
  * of every layer's X [*, d_ff], Vt [*, d_model], Y / resid [*, d_model]; layer
  * l's matrices start x/v/y/r_layer_stride ELEMENTS after layer l−1's.  Device
- * memory, σ.dtype.  rows == NULL: row i.  resid may be NULL.                 */
+ * memory, σ.dtype.  rows == NULL: row i.  resid may be NULL.  X and Vt are
+ * inputs of the whole step: fully written (on `stream`, or before it) when the
+ * call is made, not aliasing Y / resid, and not written while the step's
+ * launches run — the step's later READ launches stage their x rows before their
+ * PDL wait once its first launch has passed it (TTT_READ_EARLY_X=0: never).  */
 typedef struct {
   const void *X;
   int64_t x_layer_stride;

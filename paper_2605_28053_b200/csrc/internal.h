@@ -46,6 +46,11 @@ struct ReadParams {
   long long n_slot_layers;       // pool slots × L (third extent of the slot tensor map)
   float *ptc;                    // [2][g][⌈d_model/128⌉·128][8] fp32 partials
   size_t ptc_bytes;
+  // inside tttstate_serve_step (x_epoch > 0): X is an input of the whole step, so a launch may stage
+  // its x rows before the PDL wait once an earlier launch of the same step has passed its wait and
+  // published x_epoch in *xflag (device word; see read_decode_tc.cu)
+  int *xflag;
+  int x_epoch;
 };
 
 // a5: chunk update of one layer for every member (shadow slot <- ΔW_v + η VᵀZ).

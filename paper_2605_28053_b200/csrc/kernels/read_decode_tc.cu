@@ -88,6 +88,8 @@ struct DecTcParams {
   int early_delta;               // ΔW boxes may be requested before the PDL wait (slot-table writers never trigger early)
   int hyb;                       // the CTA's last `hyb` ΔW row blocks go to register-streaming warps, not TMA
   const __nv_bfloat16 *slots;    // slot array (the tmD tensor: [n_slot_layers][d_model][d_ff])
+  int *xflag;                    // serve_step epoch word (ReadParams::xflag)
+  int x_epoch;                   // > 0: inside tttstate_serve_step
 };
 
 template <int ID, int COUNT>
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(kTcThreads + 32 * kHybWarps, 1)
   u64 *full = bars, *empty = bars + kTcMaxStages, *t_full = bars + 2 * kTcMaxStages, *t_empty = t_full + 2;
   u64 *x_ready = t_empty + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(x_ready + 1);
-  __shared__ int s_last, s_last_h;
+  __shared__ int s_last, s_last_h, s_xe;
   __shared__ unsigned long long ts[7];
   auto stamp = [&](int i) {
     if (p.trace) {
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(kTcThreads + 32 * kHybWarps, 1)
       if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
     }
   } else if (warp == 1) {                                   // ---------------- MMA issuer
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // (reads only this CTA's shared memory and writes TMEM: no PDL wait; x_ready gates it)
     if (my_rbs > 0) {
       mbar_wait(x_ready, 0);
       if (lane == 0) stamp(1);
@@ -287,9 +289,25 @@ __global__ void __launch_bounds__(kTcThreads + 32 * kHybWarps, 1)
       }
     }
   } else if (warp < 6) {                                    // ---------------- warps 2-5
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (threadIdx.x == 64) stamp(5);
     const int q = warp & 3, et = threadIdx.x - 64;
+    // Inside tttstate_serve_step X is an input of the whole step (written before the call, never
+    // during it).  Once an earlier launch of this step has passed its PDL wait — it publishes the
+    // step's epoch in *xflag below — everything that wrote X has completed and is visible, so this
+    // launch stages its x slice before its own wait, while the previous launch drains, instead of
+    // after it with the ring already full.  Otherwise (the step's first launch, read_apply) the x
+    // loads follow the wait.
+    bool xe = false;
+    if (p.x_epoch > 0) {
+      if (et == 0) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.xflag) : "memory");
+        s_xe = v == p.x_epoch;
+      }
+      named_bar<1, 128>();
+      xe = s_xe;
+    }
+    if (!xe) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 64) stamp(5);
     const int n = p.n, dff = p.d_ff, dm = p.d_model;
     if (my_rbs > 0) {
       // x slice → shared memory, K-major 128-byte-swizzled 8-row atoms: 16-B chunk c of row r in
@@ -318,6 +336,9 @@ __global__ void __launch_bounds__(kTcThreads + 32 * kHybWarps, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes → MMA (async proxy)
       mbar_arrive(x_ready);
     }
+    if (xe) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.x_epoch > 0 && blockIdx.x == 0 && et == 0)        // this launch is past its wait: publish
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.xflag), "r"(p.x_epoch) : "memory");
     {                                                       // a4 — TailBufferUpdate, spread over every CTA
       const int zq = n * (dff / 8), gtid = blockIdx.x * 128 + et, gsz = gridDim.x * 128;
       for (int idx = gtid; idx < zq; idx += gsz) {
@@ -552,6 +573,8 @@ cudaError_t launch_read_decode_tc(const ReadParams &rp, cudaStream_t s) {
   static const int hyb = getenv("TTT_READ_TC_HYB") ? atoi(getenv("TTT_READ_TC_HYB")) : 0;
   p.hyb = ((p.nkb + p.g - 1) / p.g) * kTcBK <= kHybLd * 32 * 8 ? hyb : 0;   // (K slice within the warps' loads)
   p.slots = static_cast<const __nv_bfloat16 *>(rp.slots);
+  p.xflag = rp.xflag;
+  p.x_epoch = rp.xflag ? rp.x_epoch : 0;
   p.sel = rp.sel;
   p.X = rp.X; p.Vt = rp.Vt; p.resid = rp.resid; p.Y = rp.Y;
   p.tailZ = rp.tailZ; p.tailV = rp.tailV;

@@ -35,6 +35,7 @@ struct Layout {
   size_t members = 0;                              // MemberTable (chunk / low-rank READ groups)
   size_t wslab = 0, wtick = 0;                     // wide split-K chunk READ workspace (bf16 fast-weight)
   size_t ptc = 0, ptc_bytes = 0;                   // TMA + tcgen05 decode READ partials (bf16 fast-weight)
+  size_t xflag = 0;                                // serve_step epoch published after a READ's PDL wait
   size_t Xg = 0, Y32 = 0, U = 0, Ctr = 0, total = 0;   // low-rank READ workspace
 };
 
@@ -65,6 +66,8 @@ struct ttt_pool {
   // an event; the commit kernel writes each member's post-commit (version, sel, seq) into
   // pinned device-mapped host memory, read back only when a call needs the confirmed state
   uint64_t commit_seq = 0;
+  int step_epoch = 0;          // > 0 while tttstate_serve_step issues its launches (ReadParams::x_epoch)
+  int epoch_ctr = 0;
   std::vector<cudaEvent_t> ev_ring;                 // event recorded after commit seq k: ev_ring[k % size]
   ttt::HostOwnerState *hstate = nullptr;            // [max_owners], cudaHostAllocMapped (host view)
   ttt::HostOwnerState *hstate_dev = nullptr;        // the same memory as the kernels address it

@@ -93,6 +93,7 @@ Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt) {
   if (s.backend == TTT_FAST_WEIGHT && s.dtype == TTT_BF16) {                     // decode READ on tcgen05
     L.ptc_bytes = (size_t)2 * kTcMaxG * ((s.d_model + 127) / 128 * 128) * 8 * 4;
     L.ptc = off; off = align_up(off + L.ptc_bytes, 1024);
+    L.xflag = off; off = align_up(off + 4, 1024);
   }
   if (s.backend == TTT_FAST_WEIGHT && s.dtype == TTT_BF16 && s.chunk <= 128) {   // wide chunk READ (f2)
     L.wtick = off; off = align_up(off + (size_t)kWideMaxTiles * 4, 1024);
@@ -596,6 +597,8 @@ ttt_status read_apply_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec
     rp.n_slot_layers = (long long)(2 * p->max_owners + p->n_ckpt) * sh.n_layers;
     rp.ptc = p->lay.ptc_bytes ? reinterpret_cast<float *>(p->arena + p->lay.ptc) : nullptr;
     rp.ptc_bytes = p->lay.ptc_bytes;
+    rp.xflag = p->lay.ptc_bytes ? reinterpret_cast<int *>(p->arena + p->lay.xflag) : nullptr;
+    rp.x_epoch = rp.xflag ? p->step_epoch : 0;
     cudaError_t e = launch_read_decode(sh.dtype, rp, s);
     if (e != cudaSuccess) return cuda_fail(e, "read_decode launch");
   }
@@ -1012,6 +1015,16 @@ ttt_status tttstate_serve_step(ttt_pool *p, ttt_planner *pl, const uint64_t *own
   std::vector<OwnerRec *> recs, one;
   std::vector<int32_t> rows;
   size_t off = 0;
+  // X / Vt are inputs of the whole step: READ launches after the step's first may stage x early
+  struct EpochScope {
+    ttt_pool *p;
+    ~EpochScope() { p->step_epoch = 0; }
+  } epoch_scope{p};
+  static const bool early_x = !getenv("TTT_READ_EARLY_X") || atoi(getenv("TTT_READ_EARLY_X")) != 0;
+  if (early_x) {
+    p->epoch_ctr = p->epoch_ctr >= (1 << 30) ? 1 : p->epoch_ctr + 1;
+    p->step_epoch = p->epoch_ctr;
+  }
   for (int k = 0; k < n_groups; ++k) {
     const ttt_group &g = out->groups[k];
     if ((st = check_group(p, &g, recs)) != TTT_OK) return st;
