@@ -447,19 +447,34 @@ __global__ void __launch_bounds__(kMmaThreads, 1) read_decode_mma_kernel(const R
           (size_t)(td - m * dm) * nvec;
     load_delta(cur, row, lane);
   }
+  auto copy_x = [&]() {                           // the n x rows: one bulk copy each (no registers)
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_xbar), bytes = (uint32_t)dff * 2;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * n) : "memory");
+    for (int b = 0; b < n; ++b)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(xs + (size_t)b * nvp)),
+                   "l"(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff), "r"(bytes), "r"(bar)
+                   : "memory");
+  };
+  // inside tttstate_serve_step: once an earlier launch of the step has passed its PDL wait (it
+  // publishes the step's epoch, below), X — an input of the whole step — is complete and visible,
+  // so the bulk copies go out before this launch's wait (read_decode_tc.cu, p.x_epoch)
+  bool x_early = false;
+  if (p.xtma && p.x_epoch > 0 && tid == 0) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.xflag) : "memory");
+    if (v == p.x_epoch) {
+      copy_x();
+      x_early = true;
+    }
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (p.x_epoch > 0 && blockIdx.x == 0 && tid == 0)
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.xflag), "r"(p.x_epoch) : "memory");
   if (tid <= n) {
     if (tid == 0) {
       s_row0[0] = W;
-      if (p.xtma) {                               // the n x rows: one bulk copy each (no registers)
-        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_xbar), bytes = (uint32_t)dff * 2;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * n) : "memory");
-        for (int b = 0; b < n; ++b)
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                           (uint32_t)__cvta_generic_to_shared(xs + (size_t)b * nvp)),
-                       "l"(static_cast<const __nv_bfloat16 *>(p.X) + (size_t)p.x_row[b] * dff), "r"(bytes), "r"(bar)
-                       : "memory");
-      }
+      if (p.xtma && !x_early) copy_x();
     } else {
       const int o = p.owner_idx[tid - 1];
       s_row0[tid] = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.slots) +
