@@ -167,6 +167,8 @@ struct LowRankRead {
   int owner_idx[kMaxGroup], x_row[kMaxGroup], v_row[kMaxGroup], y_row[kMaxGroup], tail_pos[kMaxGroup];
   const void *w_down = nullptr;  // [L][d_model][d_ff] (tensor maps of the one-pass kernel)
   int L = 0, layer = 0, max_slots = 0;
+  int *xflag = nullptr;          // serve_step epoch word / epoch (ReadParams::xflag, x_epoch)
+  int x_epoch = 0;
 };
 struct LowRankWrite {
   int n, d_model, d_ff, rank, C;

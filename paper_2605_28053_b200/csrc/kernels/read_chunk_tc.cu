@@ -82,6 +82,8 @@ struct ChunkParams {
   int early_dep;                 // PDL: trigger the dependent launch at entry (TTT_CHUNK_EARLY_DEP)
   const int *owner_idx;          // device member table row 0
   LrFused lr;
+  int *xflag;                    // LR inside tttstate_serve_step: epoch word (ReadParams::xflag)
+  int x_epoch;                   //   > 0: X rows may be read before the PDL wait once published
 };
 
 __device__ __forceinline__ uint4 ld_stream(const uint4 *q) {
@@ -209,6 +211,13 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
     kb1 = nk_all * (ks + 1) / KS;
   };
 
+  // LR inside tttstate_serve_step (read_decode_tc.cu, x_epoch): once an earlier launch of the step
+  // has passed its PDL wait and published the step's epoch, X is complete and visible, and the
+  // slot table, member table and low-rank state are written only by kernels that never trigger
+  // their dependents early — so the producer (X, W_down boxes), the MMA warp (shared memory →
+  // TMEM) and the u warps' x staging and u = A x (shared memory) run before this launch's wait;
+  // every global write (tail, slabs, Bᵀu, counters) stays behind it.
+  __shared__ int s_xe;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full + s, 1);
@@ -217,12 +226,16 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
     mbar_init(t_full, 1);
     mbar_init(t_empty, 4);
     mbar_init_fence();
+    int v = 0;
+    if (LR && p.x_epoch > 0) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.xflag) : "memory");
+    s_xe = LR && p.x_epoch > 0 && v == p.x_epoch;
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const bool xe = s_xe != 0;
   // PDL: the prologue above (barriers, TMEM, tensor-map prefetch) overlaps the previous
   // kernel's tail; everything below may depend on it (X, slots, sel, workspace, counters).
   if (p.early_dep) asm volatile("griddepcontrol.launch_dependents;");
@@ -245,7 +258,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
       tma_load_3d(smem + i * STAGE + A_BYTES, &tmW, full + i, (kb0 + i) * BK, n0_of(j), p.layer);
     }
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!xe) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) stamp(1);
 
   if (warp == 0) {
@@ -300,6 +313,9 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
   } else if (warp < 6) {                                    // ---------------- epilogue warps 2-5
     const int q = warp & 3, row = q * 32 + lane;            // token index t in the chunk
     const int et = threadIdx.x - 64;
+    if (xe) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (LR && p.x_epoch > 0 && blockIdx.x == 0 && et == 0)  // past this launch's wait: publish
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.xflag), "r"(p.x_epoch) : "memory");
     int k = 0;
     for (int u = blockIdx.x; u < n_tiles; u += gridDim.x, ++k) {
       int b, j, kb0, kb1;
@@ -400,18 +416,19 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
       uint4 *tz = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.tailZ) + o * p.tz_owner + p.tz_layer +
                                             (size_t)lr.tail_pos[m] * dff);
       named_bar<3, 32 * kUW>();   // previous member's rows done
-      for (int v = ut; v < nvec; v += 32 * kUW) {    // stage x_m; a4: append z_m
-        const uint4 z = x4[v];
-        xs_lr[v] = z;
-        tz[v] = z;
-      }
-      {                                              // a4: append v_m
+      auto append_v = [&]() {                        // a4: append v_m
         const uint4 *vs = reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(p.Vt) +
                                                           (size_t)lr.v_row[m] * dm);
         uint4 *tv = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.tailV) + o * p.tv_owner + p.tv_layer +
                                               (size_t)lr.tail_pos[m] * dm);
         for (int v = ut; v < dm / 8; v += 32 * kUW) tv[v] = vs[v];
+      };
+      for (int v = ut; v < nvec; v += 32 * kUW) {    // stage x_m; a4: append z_m (after the wait if xe)
+        const uint4 z = x4[v];
+        xs_lr[v] = z;
+        if (!xe) tz[v] = z;
       }
+      if (!xe) append_v();
       named_bar<3, 32 * kUW>();   // x_m staged
       const __nv_bfloat16 *A = static_cast<const __nv_bfloat16 *>(lr.slots) + (2LL * o + p.sel[o]) * lr.slot_elems +
                                lr.layer_off;
@@ -439,6 +456,7 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
       }
       named_bar<3, 32 * kUW>();   // u_m complete (shared memory)
       if (ut == 0) stamp(4);
+      if (xe) asm volatile("griddepcontrol.wait;" ::: "memory");   // global writes from here on: behind the wait
       // Bᵀu_m: 8 outputs per thread, the R rows of B_m streamed 8 loads at a time
       const uint4 *B4 = reinterpret_cast<const uint4 *>(A + (size_t)R * dff);
       for (int i8 = ut; i8 < dm / 8; i8 += 32 * kUW) {
@@ -470,6 +488,10 @@ __global__ void __launch_bounds__(LR ? kThreadsLR : kThreads, 1)
       if (ut == 0) {
         __threadfence();
         atomicAdd(lr.ctr, 1);
+      }
+      if (xe) {                                      // a4 appends, off the u -> Bᵀu -> gate chain
+        for (int v = ut; v < nvec; v += 32 * kUW) tz[v] = xs_lr[v];
+        append_v();
       }
     }
     int b, j, kb0, kb1;                            // this CTA's (single) tile
@@ -686,6 +708,9 @@ cudaError_t launch_read_chunk(const ChunkLaunch &cl, cudaStream_t s) {
     p.tv_owner = q.tv_owner;
     p.tz_layer = q.tz_layer;
     p.tv_layer = q.tv_layer;
+    static const bool lr_early_x = !getenv("TTT_LR_EARLY_X") || atoi(getenv("TTT_LR_EARLY_X")) != 0;
+    p.xflag = q.xflag;
+    p.x_epoch = lr_early_x && cl.x_rowmap && q.xflag ? q.x_epoch : 0;   // (a gathered Xg is written in the step)
   }
   CUtensorMap mX, mW, mD;
   const bool xmap_ok = cl.x_rowmap ? cached_map(&mX, cl.X, cl.d_ff,

@@ -93,8 +93,8 @@ Layout compute_layout(const ttt_shape &s, int max_owners, int n_ckpt) {
   if (s.backend == TTT_FAST_WEIGHT && s.dtype == TTT_BF16) {                     // decode READ on tcgen05
     L.ptc_bytes = (size_t)2 * kTcMaxG * ((s.d_model + 127) / 128 * 128) * 8 * 4;
     L.ptc = off; off = align_up(off + L.ptc_bytes, 1024);
-    L.xflag = off; off = align_up(off + 4, 1024);
   }
+  L.xflag = off; off = align_up(off + 4, 1024);
   if (s.backend == TTT_FAST_WEIGHT && s.dtype == TTT_BF16 && s.chunk <= 128) {   // wide chunk READ (f2)
     L.wtick = off; off = align_up(off + (size_t)kWideMaxTiles * 4, 1024);
     L.wslab = off; off = align_up(off + kWideSlabBytes, 1024);
@@ -547,6 +547,8 @@ ttt_status read_apply_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec
     lp.L = sh.n_layers;
     lp.layer = layer;
     lp.max_slots = 2 * p->max_owners + p->n_ckpt;
+    lp.xflag = reinterpret_cast<int *>(p->arena + p->lay.xflag);
+    lp.x_epoch = p->step_epoch;
     cudaError_t e = launch_lowrank_read(lp, cl, s);
     if (e != cudaSuccess) return cuda_fail(e, "low-rank READ");
     for (int b = 0; b < g->n; ++b) {
@@ -597,8 +599,8 @@ ttt_status read_apply_recs(ttt_pool *p, const ttt_group *g, std::vector<OwnerRec
     rp.n_slot_layers = (long long)(2 * p->max_owners + p->n_ckpt) * sh.n_layers;
     rp.ptc = p->lay.ptc_bytes ? reinterpret_cast<float *>(p->arena + p->lay.ptc) : nullptr;
     rp.ptc_bytes = p->lay.ptc_bytes;
-    rp.xflag = p->lay.ptc_bytes ? reinterpret_cast<int *>(p->arena + p->lay.xflag) : nullptr;
-    rp.x_epoch = rp.xflag ? p->step_epoch : 0;
+    rp.xflag = reinterpret_cast<int *>(p->arena + p->lay.xflag);
+    rp.x_epoch = p->step_epoch;
     cudaError_t e = launch_read_decode(sh.dtype, rp, s);
     if (e != cudaSuccess) return cuda_fail(e, "read_decode launch");
   }
