@@ -7,7 +7,9 @@ with plain loads instead of the L2 evict_last / evict_first hints (TTT_READ_L2KE
 serial-order READ, and both chunk READ kernels on every shape (TTT_CHUNK_WIDE=1 forces the wide
 split-K kernel wherever it has a plan, =0 keeps the narrow one at paper dims), and the SIMT
 decode READ with the mma.sync base (TTT_READ_TC=0; the default is the TMA + tcgen05 READ), and
-the TMA + tcgen05 READ with its last ΔW row blocks streamed by register warps (TTT_READ_TC_HYB)."""
+the TMA + tcgen05 READ with its last ΔW row blocks streamed by register warps (TTT_READ_TC_HYB),
+and every READ with its x rows loaded after the PDL wait only (TTT_READ_EARLY_X=0,
+TTT_LR_EARLY_X=0; the default stages them early inside a serve_step)."""
 import os
 import subprocess
 import sys
@@ -39,6 +41,8 @@ def _run(env_extra, target):
     ({"TTT_CHUNK_WIDE": "0"}, "tests/test_gpu_full_size.py::test_f2_chunk_read_paper_dims"),
     ({"TTT_READ_TC_HYB": "2"}, "tests/test_gpu_parity.py"),
     ({"TTT_READ_TC_HYB": "1"}, "tests/test_gpu_paper_dims.py"),
+    ({"TTT_READ_EARLY_X": "0"}, "tests/test_gpu_configs.py"),
+    ({"TTT_LR_EARLY_X": "0"}, "tests/test_gpu_lowrank.py"),
 ])
 def test_alternative_paths_parity(env, target):
     _run(env, target)
