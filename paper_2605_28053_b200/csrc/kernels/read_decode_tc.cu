@@ -34,10 +34,15 @@
 // stream; ncu tensor pipe 3.8 %, so not MMA throughput); 2 / 3 / 4 boxes per stage: 77.6 / 76.6 /
 // 78.3 µs in tools/microbench.py.  In bench.py (the 36-layer decode window) it beats the SIMT
 // kernel read_decode_mma_kernel: 74.0–74.3 vs 74.7–76.9 µs per launch on power-capped boxes,
-// 73.9 µs = 0.929 of HBM in the final run, so it is the default bf16 decode READ for
+// 73.9 µs = 0.929 of HBM at full clock, so it is the default bf16 decode READ for
 // groups that fit one launch (≤ 8 members).  Groups split over several launches (configs 3 / 5)
 // keep the SIMT kernel, measured faster there; TTT_READ_TC=0 restores it everywhere; fp32 pools
 // and the fused C = 1 READ+WRITE always use it.
+//
+// Early x (inside tttstate_serve_step): a launch whose step epoch is already published
+// stages its x slice before the PDL wait, and the MMA warp never waits (shared memory → TMEM
+// only), so the preloaded ring drains while the previous launch finishes: 72.6 µs = 0.945 of HBM
+// in bench.py on a power-capped 1,770 MHz box (3,022 vs 2,946 tok/s without it, same box).
 //
 // TTT_READ_TC_HYB = h (opt-in, measured not kept): warps 6–9 stream the CTA's last h ΔW row blocks
 // through registers next to the TMA ring (more bytes in flight per SM).  h = 1 / 2 / 3: 74.8 / 76.6 /
