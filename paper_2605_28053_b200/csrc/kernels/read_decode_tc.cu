@@ -95,6 +95,7 @@ struct DecTcParams {
   const __nv_bfloat16 *slots;    // slot array (the tmD tensor: [n_slot_layers][d_model][d_ff])
   int *xflag;                    // serve_step epoch word (ReadParams::xflag)
   int x_epoch;                   // > 0: inside tttstate_serve_step
+  int runahead;                  // producer streams past the ring fill before the PDL wait (early_delta only)
 };
 
 template <int ID, int COUNT>
@@ -233,11 +234,14 @@ __global__ void __launch_bounds__(kTcThreads + 32 * kHybWarps, 1)
         for (int kb = kb_lo; kb < kb_hi; kb += p.bps, ++it) {   // a stage = bps boxes (consecutive K blocks)
           const int s = it % S, nb = min(p.bps, kb_hi - kb);
           if (it >= p.pre || it >= S) {
-            if (!waited) {                                   // (pre-wait prefetch budget used: wait now)
+            // (pre-wait prefetch budget used: wait now — unless nothing this producer loads can be
+            // written by an earlier grid: W_down never, ΔW slots only by kernels that never
+            // trigger early (p.early_delta); TTT_READ_TC_RUNAHEAD=0 keeps the wait)
+            if (!waited && !(p.runahead && p.early_delta)) {
               asm volatile("griddepcontrol.wait;" ::: "memory");
               waited = true;
             }
-            mbar_wait(empty + s, ((it / S) - 1) & 1);
+            if (it >= S) mbar_wait(empty + s, ((it / S) - 1) & 1);
           }
           mbar_expect_tx(full + s, (uint32_t)nb * kTcBoxBytes);
           for (int i = 0; i < nb; ++i) {
@@ -251,7 +255,7 @@ __global__ void __launch_bounds__(kTcThreads + 32 * kHybWarps, 1)
           }
         }
       }
-      if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (!waited && !(p.runahead && p.early_delta)) asm volatile("griddepcontrol.wait;" ::: "memory");
     }
   } else if (warp == 1) {                                   // ---------------- MMA issuer
     // (reads only this CTA's shared memory and writes TMEM: no PDL wait; x_ready gates it)
@@ -579,6 +583,8 @@ cudaError_t launch_read_decode_tc(const ReadParams &rp, cudaStream_t s) {
   p.hyb = ((p.nkb + p.g - 1) / p.g) * kTcBK <= kHybLd * 32 * 8 ? hyb : 0;   // (K slice within the warps' loads)
   p.slots = static_cast<const __nv_bfloat16 *>(rp.slots);
   p.xflag = rp.xflag;
+  static const int runahead = getenv("TTT_READ_TC_RUNAHEAD") ? atoi(getenv("TTT_READ_TC_RUNAHEAD")) : 1;
+  p.runahead = runahead;
   p.x_epoch = rp.xflag ? rp.x_epoch : 0;
   p.sel = rp.sel;
   p.X = rp.X; p.Vt = rp.Vt; p.resid = rp.resid; p.Y = rp.Y;
