@@ -806,10 +806,12 @@ cudaError_t launch_read_decode(int dtype, const ReadParams &p, cudaStream_t s) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist_mb << 20);
     limit_set = true;
   }
-  // the TMA + tcgen05 READ for groups that fit one launch (bench.py config 2: 74.3 vs 75.7-76.9 µs);
-  // groups split over several launches keep the SIMT kernel, which measured faster there
-  // (configs 3 / 5: 0.84 / 0.83 vs 0.81 / 0.80 of the roofline with the TMA READ)
-  if (p.kc > 0 && !p.fuse && !p.l2keep && p.ptc && read_decode_tc_supported(p.n, p.d_model, p.d_ff)) {
+  // the TMA + tcgen05 READ for every bf16 group (bench.py config 2: 68.8 vs 75.7-76.9 µs).  Groups
+  // split over several launches (configs 3 / 5) kept the SIMT kernel while the TMA READ stopped at
+  // the PDL wait (0.81 / 0.80 vs 0.84 / 0.83 of the roofline); with its producer streaming past the
+  // wait it is faster there too: 0.883 / 0.865 vs 0.853 / 0.841 (TTT_READ_TC_MULTI=0: SIMT for them)
+  static const int tc_multi = getenv("TTT_READ_TC_MULTI") ? atoi(getenv("TTT_READ_TC_MULTI")) : 1;
+  if (p.kc > 0 && !p.fuse && (!p.l2keep || tc_multi) && p.ptc && read_decode_tc_supported(p.n, p.d_model, p.d_ff)) {
     static const int early_delta = getenv("TTT_READ_EARLY_DELTA") ? atoi(getenv("TTT_READ_EARLY_DELTA")) : 1;
     ReadParams q = p;
     q.early_delta = early_delta && !write_tc_triggers_early();

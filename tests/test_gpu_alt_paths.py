@@ -42,6 +42,7 @@ def _run(env_extra, target):
     ({"TTT_READ_TC_HYB": "2"}, "tests/test_gpu_parity.py"),
     ({"TTT_READ_TC_HYB": "1"}, "tests/test_gpu_paper_dims.py"),
     ({"TTT_READ_EARLY_X": "0"}, "tests/test_gpu_configs.py"),
+    ({"TTT_READ_TC_MULTI": "0"}, "tests/test_gpu_configs.py"),
     ({"TTT_READ_TC_RUNAHEAD": "0", "TTT_READ_EARLY_X": "0"}, "tests/test_gpu_parity.py"),
     ({"TTT_LR_EARLY_X": "0"}, "tests/test_gpu_lowrank.py"),
 ])
