@@ -36,7 +36,9 @@
 // kernel read_decode_mma_kernel: 74.0–74.3 vs 74.7–76.9 µs per launch on power-capped boxes,
 // 73.9 µs = 0.929 of HBM at full clock, so it is the default bf16 decode READ for
 // groups that fit one launch (≤ 8 members).  Groups split over several launches (configs 3 / 5)
-// keep the SIMT kernel, measured faster there; TTT_READ_TC=0 restores it everywhere; fp32 pools
+// kept the SIMT kernel (faster there) until the producer streamed past the PDL wait (below); now
+// this kernel serves them too (0.883 / 0.865 vs 0.853 / 0.841 of the roofline).  TTT_READ_TC=0
+// restores the SIMT kernel everywhere, TTT_READ_TC_MULTI=0 for multi-launch groups; fp32 pools
 // and the fused C = 1 READ+WRITE always use it.
 //
 // Early x (inside tttstate_serve_step): a launch whose step epoch is already published
