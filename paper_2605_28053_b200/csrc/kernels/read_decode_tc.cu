@@ -21,7 +21,7 @@
 // round-robin to G groups of g CTAs; CTA `sub` of a group streams K blocks [sub·nkb/g,
 // (sub+1)·nkb/g) of each of its group's row blocks, so its slice of the x rows is staged in shared
 // memory once.  plan_g picks g to minimise the busiest CTA's boxes, then the smallest x slice
-// (most ring stages): at paper dims g = 8, G = 18 (144 CTAs, 10 row blocks × 19 K blocks each).
+// (most ring stages) and most SMs: at paper dims g = 7, G = 21 (147 CTAs, ≤ 9 row blocks × 22 K blocks).
 // Each (row block, K slice) partial goes to a workspace slab; the last of the (1+n)·g arrivals
 // for an output row block (per-row-block ticket) sums, in a fixed order, Σ_slices W-partial[b] +
 // Σ_slices ΔW_b-partial (+ resid) → bf16 y (deterministic).  Warps: 0 TMA producer (lane 0),
@@ -493,27 +493,40 @@ __global__ void __launch_bounds__(kTcThreads + 32 * kHybWarps, 1)
   }
 }
 
-// g (CTAs per row block) minimising the K blocks of the busiest CTA, ⌈rbs / G⌉ · ⌈nkb / g⌉;
-// among equals the smallest x slice (8 rows × its K blocks × 128 B), which leaves the most ring
-// stages: a box's slot is held until its MMAs complete, so bytes in flight = ring − slots in MMA.
+// g (CTAs per row block): first the K blocks of the busiest CTA, ⌈rbs / G⌉ · ⌈nkb / g⌉, are
+// minimised; then, among the g within 5 % of that minimum whose ring is as deep as any (a box's
+// slot is held until its MMAs complete, so bytes in flight = ring − slots in MMA), the one that
+// streams on the most SMs (G · g).  Since the producer streams past the PDL wait, consecutive
+// launches overlap and a CTA that finishes early starts the next launch's boxes, so the SMs in use
+// count more than the last CTA of one launch: at paper dims g = 7 (147 SMs, busiest CTA 198
+// boxes) measured 3,194–3,198 tok/s vs 3,152 for g = 8 (144 SMs, 190 boxes), g = 5 / 6 3,174–3,190;
+// g = 10 / 12 (row blocks of 16 / 13 boxes: the per-row-block epilogue no longer hides) 2,824–2,942.
 int plan_g(int n_rb, int nkb, int sms, int *G_out, int *stages_out) {
-  int best = 0, best_cost = 1 << 30, best_st = 0;
   static const int st_env = getenv("TTT_READ_TC_STAGES") ? atoi(getenv("TTT_READ_TC_STAGES")) : kTcMaxStages;
-  for (int g = 1; g <= std::min({sms, nkb, kTcMaxG}); ++g) {     // (kTcMaxG: the partials workspace)
-    const int G = sms / g, nkq = (nkb + g - 1) / g;
-    const int st = std::min(st_env, (int)((227 * 1024 - 4096 - (size_t)nkq * 1024) / kTcBoxBytes));
-    if (st < 4) continue;
-    const int cost = ((n_rb + G - 1) / G) * nkq;
-    if (cost < best_cost || (cost == best_cost && st > best_st)) {
-      best_cost = cost;
+  const int gmax = std::min({sms, nkb, kTcMaxG});                  // (kTcMaxG: the partials workspace)
+  auto stages_of = [&](int g) {
+    const int nkq = (nkb + g - 1) / g;
+    return std::min(st_env, (int)((227 * 1024 - 4096 - (size_t)nkq * 1024) / kTcBoxBytes));
+  };
+  auto cost_of = [&](int g) { const int G = sms / g; return ((n_rb + G - 1) / G) * ((nkb + g - 1) / g); };
+  int best_cost = 1 << 30, best_st = 0;
+  for (int g = 1; g <= gmax; ++g)
+    if (stages_of(g) >= 4) best_cost = std::min(best_cost, cost_of(g));
+  if (best_cost == 1 << 30) return 0;
+  for (int g = 1; g <= gmax; ++g)
+    if (stages_of(g) >= 4 && cost_of(g) * 100 <= best_cost * 105) best_st = std::max(best_st, stages_of(g));
+  int best = 0, best_used = 0, best_c = 1 << 30;
+  for (int g = 1; g <= gmax; ++g) {
+    if (stages_of(g) != best_st || cost_of(g) * 100 > best_cost * 105) continue;
+    const int G = sms / g, used = std::min(G, n_rb) * g, c = cost_of(g);
+    if (used > best_used || (used == best_used && c < best_c)) {
       best = g;
-      best_st = st;
+      best_used = used;
+      best_c = c;
     }
   }
-  if (best) {
-    *G_out = sms / best;
-    *stages_out = best_st;
-  }
+  *G_out = sms / best;
+  *stages_out = best_st;
   return best;
 }
 
