@@ -586,6 +586,7 @@ def main():
                          "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "alg_bytes_per_launch": read_bytes, "avg_launch_ms": read_avg,
                          "launches_timed": len(read_ms), "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                         "peak_note": "a copy (read + write) figure; this kernel only reads, and a read-only TMA stream measured 6.8 TB/s (tools/tma_tensor_probe.cu), so frac can exceed 1",
                          "timing": "CUDA events on the launch stream around the L back-to-back READ launches of "
                                    "every 8th decode step of the timed region; avg = span / L"},
             "write": {"kernel": "write_commit (a5+a6, all layers)", "avg_call_ms": write_avg,
