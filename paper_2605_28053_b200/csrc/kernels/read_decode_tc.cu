@@ -46,6 +46,12 @@
 // only), so the preloaded ring drains while the previous launch finishes: 72.6 µs = 0.945 of HBM
 // in bench.py on a power-capped 1,770 MHz box (3,022 vs 2,946 tok/s without it, same box).
 //
+// Run-ahead: the producer does not stop at the PDL wait once its ring is full — W_down is never
+// written and ΔW slots only by kernels that never trigger early (p.early_delta) — so it streams on
+// while the MMA warp fills both TMEM buffers; only the epilogue's global writes wait.  72.5 → 68.8
+// µs per launch (3,020 → 3,186 tok/s); with the g = 7 plan 68.5 µs = the measured HBM copy peak
+// (TTT_READ_TC_RUNAHEAD=0: stop at the wait).
+//
 // TTT_READ_TC_HYB = h (opt-in, measured not kept): warps 6–9 stream the CTA's last h ΔW row blocks
 // through registers next to the TMA ring (more bytes in flight per SM).  h = 1 / 2 / 3: 74.8 / 76.6 /
 // 87.4 µs per launch vs 74.2–75.4 default on the same box — the launch is DRAM-rate bound here.
